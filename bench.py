@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py — MPPI rollout timesteps/s (K*T per s) and control-update latency on B200.
+
+One "step" = one full MPPI optimisation (Alg. 1 :356-368): Philox noise -> rollouts
+-> [NCCL MIN] -> weights + weighted noise sum -> [NCCL SUM] -> U update, over K_global samples.
+Default workload: BASELINE config C5 (quadrotor, 50-cylinder 4 m forest, T=200) at K = 2^22,
+strong-scaled over N GPUs (each rank rolls out K/N samples).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C5]
+  torchrun --nproc-per-node N bench.py --gpus N ...       (N > 1; NCCL over NVLink)
+
+Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement" for every field.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MPPI rollout timesteps/sec (K*T per s)"
+UNIT = "K*T/s"
+
+# FP32 FLOPs per sample-step of the rollout kernel (FADD + FMUL + 2 FFMA + 2 FADD2 + 2 FMUL2 +
+# 4 FFMA2 per thread, ncu sass counters / (K*T)); see DESIGN.md "Rollout FLOPs".  None -> not
+# yet measured for that plant (roofline falls back to the kernel's measured share only).
+ROLLOUT_FLOP_PER_SS = {"cartpole": None, "racecar": None, "quadrotor": None}
+
+SM_COUNT_B200 = 148
+FP32_LANES_PER_SM = 128
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="C5")
+    p.add_argument("--K", type=int, default=0, help="global samples (default: the config's)")
+    p.add_argument("--no-latency", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-probe", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=5)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def fp32_peak(probe_ok, sm_count, sm_max_mhz):
+    derived = sm_count * FP32_LANES_PER_SM * 2 * sm_max_mhz * 1e6 / 1e12
+    out = {"derived_tflops": derived, "ffma_probe_tflops": None, "ffma2_probe_tflops": None}
+    if probe_ok:
+        try:
+            from paper_1509_01149_b200 import probe_build
+            out["ffma_probe_tflops"] = probe_build.probe(False)[0]
+            out["ffma2_probe_tflops"] = probe_build.probe(True)[0]
+        except Exception as e:  # the probe is context for the denominator, never the product
+            out["probe_error"] = str(e)[:200]
+    cands = [v for k, v in out.items() if k.endswith("tflops") and v]
+    out["peak_tflops"] = max(cands)
+    return out
+
+
+def cpu_baseline(w, steps=1, k_sample=None):
+    """The fp64 oracle (as it stands) on this host's cores, on a bounded sample of the workload."""
+    import numpy as np
+    from oracle import oracle as O
+    cores = len(os.sched_getaffinity(0))
+    K = k_sample or min(w.K, 1 << 16)
+    pb = O.Problem(w.plant, T=w.T, dt=w.dt, lam=w.lam, nu=w.nu, Sigma=w.Sigma, R=w.R,
+                   obstacles=w.obstacles if w.plant == "quadrotor" else None)
+    U = w.U0.astype(np.float64)
+    t0 = time.perf_counter()
+    for s in range(steps):
+        eps = O.noise(w.seed, s, w.T, K, w.m)
+        r = O.optimize(pb, w.x0, U, eps, nthreads=cores)
+        U = r["U"]
+    dt = time.perf_counter() - t0
+    return {"value": K * w.T * steps / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": "%d step(s) of %s at K=%d (of %d), T=%d: noise + rollouts (OpenMP over k) "
+                      "+ k-ordered reduction, fp64" % (steps, w.name, K, w.K, w.T),
+            "seconds": dt}
+
+
+def lscpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """--impl reference: the oracle timed on the host cores, same metric/config."""
+    if rank != 0:
+        return 0
+    from mppi_inputs import get
+    w = get(args.config)
+    ksamp = min(w.K, 1 << 14)
+    for _ in range(args.warmup):
+        cpu_baseline(w, steps=1, k_sample=min(ksamp, 1024))
+    r = cpu_baseline(w, steps=args.steps, k_sample=ksamp)
+    line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * r["seconds"] / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "%s (oracle sample K=%d per step)" % (w.name, ksamp),
+                       "plant": w.plant, "K": w.K, "T": w.T},
+            "impl": "reference",
+            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
+                             "sample": r["sample"], "cpu": lscpu_model()},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- latency
+def latency(cfg_name, iters=200, warm=20):
+    import torch
+    from mppi_inputs import get
+    from paper_1509_01149_b200 import from_workload
+    w = get(cfg_name)
+    m = from_workload(w)
+    U = torch.tensor(w.U0, device="cuda")
+    for i in range(warm):
+        m.optimize(w.x0, U, w.seed, i)
+    torch.cuda.synchronize()
+    dev, host = [], []
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for i in range(iters):
+        t0 = time.perf_counter()
+        evs[i][0].record()
+        m.optimize(w.x0, U, w.seed, warm + i)
+        evs[i][1].record()
+        u0 = U[0].cpu()                       # control to send to the actuators (4 m bytes D2H)
+        host.append((time.perf_counter() - t0) * 1e6)
+    torch.cuda.synchronize()
+    dev = [a.elapsed_time(b) * 1e3 for a, b in evs]
+    del u0
+    q = lambda xs, p: sorted(xs)[min(len(xs) - 1, int(round(p * (len(xs) - 1))))]
+    launches = m.last_launch_count()
+    m.close()
+    return {"K": w.K, "T": w.T, "plant": w.plant, "device_us_p50": q(dev, 0.5),
+            "device_us_p99": q(dev, 0.99), "host_us_p50": q(host, 0.5), "host_us_p99": q(host, 0.99),
+            "calls": iters, "kernels_per_call": launches,
+            "KT_per_s_at_p50": w.K * w.T / (q(dev, 0.5) * 1e-6)}
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    args = parse_args()
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from mppi_inputs import get
+    from paper_1509_01149_b200 import ShardedMPPI, from_workload
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = get(args.config)
+    K = args.K or w.K
+    m = from_workload(w, K=K, rank=rank, world=world)
+    U = torch.tensor(w.U0, device="cuda")
+    sh = ShardedMPPI(m) if world > 1 else None
+
+    def step(i, Ut):
+        if sh is None:
+            m.optimize(w.x0, Ut, w.seed, i)
+        else:
+            sh.optimize(w.x0, Ut, w.seed, i)
+
+    for i in range(args.warmup):
+        step(i, U)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    m.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record()
+    for i in range(args.steps):
+        step(args.warmup + i, U)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    ktimes = m.profile_read()
+    m.profile_enable(False)
+    clk = clocks.stop()
+    launches = sum(v[1] for v in ktimes.values())
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        lt = torch.tensor([launches], device="cuda", dtype=torch.int64)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+        launches = int(lt.item())
+    assert torch.isfinite(U).all(), "U diverged"
+    value = K * w.T * args.steps / (ms * 1e-3)
+
+    # ---- e2e through the public API from host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        Uh = np.ascontiguousarray(w.U0.copy())
+        h2d = w.T * w.m * 4 + w.n * 4
+        d2h = w.T * w.m * 4
+        if world == 1:
+            for i in range(2):
+                m.optimize_host(w.x0, Uh, w.seed, i)
+            t0 = time.perf_counter()
+            for i in range(args.steps):
+                m.optimize_host(w.x0, Uh, w.seed, args.warmup + i)
+            el = time.perf_counter() - t0
+        else:
+            Up = torch.tensor(w.U0).pin_memory()
+            Ud = torch.empty_like(U)
+            dist.barrier()
+            t0 = time.perf_counter()
+            for i in range(args.steps):
+                Ud.copy_(Up, non_blocking=True)
+                sh.optimize(w.x0, Ud, w.seed, args.warmup + i)
+                Up.copy_(Ud, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+            el = time.perf_counter() - t0
+            t = torch.tensor([el], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": K * w.T * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * el / args.steps,
+               "api": "mppi_optimize_host" if world == 1 else "ShardedMPPI.optimize + pinned copies"}
+
+    if rank != 0:
+        m.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (rank 0's launches, CUDA events on its stream)
+    pk = measured_peaks()
+    props = torch.cuda.get_device_properties(local)
+    sm_max = (clk or {}).get("sm_max_mhz") or pk.get("sm_max_mhz", 1965.0)
+    kern = {k: {"avg_ms": v[0] / v[1] if v[1] else None, "launches": v[1], "share": None}
+            for k, v in ktimes.items()}
+    tot = sum(v[0] for v in ktimes.values()) or 1.0
+    for k, v in ktimes.items():
+        kern[k]["share"] = v[0] / tot
+    dom = max(ktimes, key=lambda k: ktimes[k][0])
+    avg_s = kern[dom]["avg_ms"] * 1e-3
+    K_loc = K // world
+    roof = {"kernel": dom}
+    if dom == "rollout":
+        fp = fp32_peak(not args.no_probe, props.multi_processor_count, sm_max)
+        fl = ROLLOUT_FLOP_PER_SS.get(w.plant)
+        ach = fl * K_loc * w.T / avg_s / 1e12 if fl else None
+        roof.update({"bound": "alu", "achieved": ach, "peak": fp["peak_tflops"], "unit": "TFLOP/s",
+                     "frac": ach / fp["peak_tflops"] if ach else None, "traffic": None,
+                     "flop_per_sample_step": fl, "peak_detail": fp})
+    else:
+        algo = 4.0 * w.T * K_loc * w.m + 4.0 * K_loc if dom == "wsum" else 4.0 * w.T * K_loc * w.m
+        peak = pk.get("hbm_gbs", 6650.0)
+        ach = algo / avg_s / 1e9
+        roof.update({"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": None, "algorithmic_bytes_per_launch": algo,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"})
+    # secondary rooflines: the HBM-bound reduction and noise kernels
+    extra = {}
+    if kern["wsum"]["avg_ms"]:
+        b = 4.0 * w.T * K_loc * w.m + 4.0 * K_loc
+        extra["wsum_hbm_GBps"] = b / (kern["wsum"]["avg_ms"] * 1e-3) / 1e9
+        extra["wsum_hbm_frac"] = extra["wsum_hbm_GBps"] / pk.get("hbm_gbs", 6650.0)
+    if kern["noise"]["avg_ms"]:
+        b = 4.0 * w.T * K_loc * w.m
+        extra["noise_write_GBps"] = b / (kern["noise"]["avg_ms"] * 1e-3) / 1e9
+    roof["secondary"] = extra
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_baseline(w)
+            cpu["cpu"] = lscpu_model()
+        except Exception as e:
+            cpu = {"error": str(e)[:200]}
+
+    lat = None
+    if not args.no_latency and world == 1:
+        lat = {c: latency(c) for c in ("C1", "C2")}
+
+    eps_bytes = 4 * w.T * K_loc * w.m
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Philox noise, committed 4 m cylinder forest, paper cost weights)",
+        "config": {"workload": "%s: %s K=%d T=%d m=%d nu=%g lambda=%g (K/N per GPU)"
+                   % (args.config, w.plant, K, w.T, w.m, w.nu, w.lam),
+                   "K": K, "K_per_gpu": K_loc, "T": w.T, "n_obstacles": int(len(w.obstacles)),
+                   "l2": "inputs larger than L2 (noise %.1f GB per GPU per step)" % (eps_bytes / 1e9),
+                   "parallelism": "K-sharded dp%d, NCCL MIN + SUM allreduce" % world},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clk, "kernels": kern, "latency": lat,
+        "device": torch.cuda.get_device_name(local),
+    }
+    print(json.dumps(line), flush=True)
+    m.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

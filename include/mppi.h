@@ -1,0 +1,338 @@
+/*
+ * mppi.h — C ABI of libmppi_b200.so: one Model Predictive Path Integral (MPPI)
+ * optimisation step on an NVIDIA B200 (sm_100a), after
+ *   G. Williams, A. Aldrich, E. Theodorou, "Model Predictive Path Integral Control
+ *   using Covariance Variable Importance Sampling", arXiv:1509.01149.
+ *
+ * The step (Algorithm 1; update law Eq. App_PI, :318-321):
+ *   1. draw eps[t][k] ~ N(0, I_m)
+ *   2. du[t][k] = sqrt(nu) * L * eps[t][k], L = chol(Sigma) (PAPER.md:308 A = sqrt(nu) I, :312)
+ *   3. roll out x_{t+1} = x_t + F(x_t, U_t + du_t) * dt
+ *      accumulating S~_k = sum_t q~ with
+ *      q~ = q(x_{t+1}) + (1 - 1/nu)/2 du'R du + U_t'R du + 1/2 U_t'R U_t
+ *   4. S_min = min_k S~_k, w_k = exp(-(S~_k - S_min)/lambda), eta = sum_k w_k
+ *   5. U_t += sum_k w_k du[t][k] / eta
+ *
+ * Conventions for every entry point:
+ *   - Device pointers are CUDA global-memory addresses on the context's device; host
+ *     pointers are ordinary CPU memory.  Each argument says which.
+ *   - Every call is ASYNCHRONOUS on the context's stream unless stated otherwise:
+ *     MPPI_OK means "validated and enqueued".  Errors of kernels already enqueued
+ *     surface as MPPI_ERR_CUDA on a later call.
+ *   - A context is single-owner and not thread-safe: one call at a time.
+ *   - Floating-point buffers are fp32, row-major, densely packed.
+ *   - Layouts: U is [T][m]; eps (noise) is [T][K_loc][m] (sample-contiguous rows so that
+ *     per-timestep reads across samples coalesce); costs is [K_loc].
+ *   - On error the call returns a non-zero status, enqueues nothing, and
+ *     mppi_last_error() returns a thread-local description.
+ *   - There is no CPU fallback: without a usable CUDA device mppi_create fails with
+ *     MPPI_ERR_CUDA.
+ */
+#ifndef MPPI_B200_H
+#define MPPI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPPI_ABI_VERSION 1
+
+typedef enum {
+    MPPI_OK = 0,
+    MPPI_ERR_INVALID_ARG = 1,  /* bad size, pointer, non-finite or out-of-range scalar */
+    MPPI_ERR_NOT_SPD = 2,      /* Sigma or R is not symmetric positive definite (fp64 Cholesky) */
+    MPPI_ERR_OOM = 3,          /* device or pinned-host allocation failed */
+    MPPI_ERR_CUDA = 4,         /* CUDA runtime error (no device, launch failure, async fault) */
+    MPPI_ERR_UNSUPPORTED = 6   /* valid request outside what this build implements */
+} mppi_status_t;
+
+typedef enum {
+    MPPI_PLANT_CARTPOLE = 1,   /* PAPER.md:395 (§V-A); n = 4, m = 1 */
+    MPPI_PLANT_RACECAR = 2,    /* PAPER.md:398 (§V-B); n = 6, m = 2 */
+    MPPI_PLANT_QUADROTOR = 3,  /* PAPER.md:422, :431-433 (§V-C); n = 16, m = 4 */
+    MPPI_PLANT_LINEAR = 4      /* linear test plant x' = A x + B v, q = x'Qx; n <= 8, m <= 4 */
+} mppi_plant_t;
+
+/* ---------------------------------------------------------------- dynamics (F of the Euler step) */
+
+/* Cart-pole, state [p, p', theta, theta'], control u = desired cart velocity.
+ * p'' = vel_gain (u - p')                            (vel_gain = 10)
+ * theta'' = -(g/l) sin theta - (p''/l) cos theta,  theta = 0 hanging */
+typedef struct {
+    float g;             /* 9.81 */
+    float pole_length;   /* 1.0 */
+    float vel_gain;      /* 10.0 */
+} mppi_cartpole_dynamics_t;
+
+/* Race car, state [X, Y, psi, vx, vy, r], control [delta (steer, rad), tau (throttle)].
+ * Single-track model with Pacejka lateral tires (the paper's
+ * [HindThesis] model is unavailable).  delta and tau saturate inside F.
+ *   D_f = mu m g lr/(lf+lr), D_r = mu m g lf/(lf+lr), vbar = max(vx, v_min)
+ *   alpha_f = delta - atan((vy + lf r)/vbar), alpha_r = -atan((vy - lr r)/vbar)
+ *   F_yf = D_f sin(C atan(B alpha_f)), F_yr = D_r sin(C atan(B alpha_r))
+ *   F_x  = Cm tau - Cr vx - Cd vx|vx|
+ *   X' = vx cos psi - vy sin psi, Y' = vx sin psi + vy cos psi, psi' = r
+ *   vx' = (F_x - F_yf sin delta)/m + vy r, vy' = (F_yr + F_yf cos delta)/m - vx r
+ *   r'  = (lf F_yf cos delta - lr F_yr)/Iz */
+typedef struct {
+    float mass, Iz, lf, lr;
+    float tire_B, tire_C, mu;
+    float Cm, Cr, Cd;
+    float v_min, g;
+    float steer_max;                 /* |delta| <= steer_max */
+    float throttle_min, throttle_max;
+} mppi_racecar_dynamics_t;
+
+/* Quadrotor, state [p(3), v(3), phi, theta, psi (ZXY Euler), p, q, r (body rates),
+ * F1..F4 (rotor thrusts)], control = 4 thrust commands saturated to [thrust_min, thrust_max].
+ * GRASP structure:
+ *   v' = (sum F / mass) R(phi,theta,psi) e3 - g e3,  R = Rz(psi) Rx(phi) Ry(theta)
+ *   phi' = c_th p + s_th r;  psi' = (-s_th p + c_th r)/chat, chat = copysign(max(|c_phi|, cos_phi_min), c_phi)
+ *   theta' = q - s_phi psi'
+ *   I w' = [arm (F2 - F4), arm (F3 - F1), yaw_coeff (F1 - F2 + F3 - F4)] - w x I w
+ *   F_i' = motor_gain (sat(u_i) - F_i) */
+typedef struct {
+    float mass, arm;
+    float Ixx, Iyy, Izz;
+    float yaw_coeff, motor_gain, g;
+    float thrust_min, thrust_max;
+    float cos_phi_min;
+} mppi_quadrotor_dynamics_t;
+
+/* Linear test plant: x' = A x + B v, A [n][n], B [n][m] row-major. */
+typedef struct {
+    int32_t n;           /* 1..8 */
+    float A[64];
+    float B[32];
+} mppi_linear_dynamics_t;
+
+typedef struct {
+    uint32_t struct_size;            /* sizeof(mppi_dynamics_t) */
+    mppi_plant_t plant;
+    union {
+        mppi_cartpole_dynamics_t cartpole;
+        mppi_racecar_dynamics_t racecar;
+        mppi_quadrotor_dynamics_t quadrotor;
+        mppi_linear_dynamics_t linear;
+    } p;
+} mppi_dynamics_t;
+
+/* ---------------------------------------------------------------- state cost q(x) */
+
+/* q = w_p p^2 + w_theta (1 + cos theta)^2 + w_thetadot theta'^2 + w_pdot p'^2
+ * (paper: 1, 500, 1, 1) */
+typedef struct {
+    float w_p, w_theta, w_thetadot, w_pdot;
+} mppi_cartpole_cost_t;
+
+/* q = w_track d^2 + w_speed (vx - v_ref)^2, d = |(X/a)^2 + (Y/b)^2 - 1|
+ * (paper: 100, 1, v_ref = 7, a = 13, b = 6) */
+typedef struct {
+    float track_a, track_b;
+    float w_track, w_speed, v_ref;
+} mppi_racecar_cost_t;
+
+/* q = w_xy((px-gx)^2 + (py-gy)^2) + w_z (pz-gz)^2 + w_yaw psi^2 + w_vel |v|^2
+ *                 + w_obs exp(-d / obs_length) + w_crash C
+ * (paper: 2.5, 150, 50, 1, 350, 12, 1000).  d = distance from (px, py) to the nearest
+ * cylinder surface, max(0, |p - c_j| - obstacle_radius); d = +inf with no
+ * obstacles.  C = 1 once pz <= ground_z or d <= 0; C is sticky and freezes the state for the
+ * rest of the rollout; the frozen state keeps being charged every step. */
+typedef struct {
+    float goal[3];
+    float w_xy, w_z, w_yaw, w_vel;
+    float w_obs, obs_length, w_crash;
+    float ground_z;
+    float obstacle_radius;           /* one radius for every cylinder */
+    int32_t n_obstacles;             /* 0..MPPI_MAX_OBSTACLES */
+    const float* obstacles_xy;       /* HOST [n_obstacles][2] cylinder centres; copied at create */
+} mppi_quadrotor_cost_t;
+
+#define MPPI_MAX_OBSTACLES 4096
+
+/* Linear test plant: q = x'Q x, Q [n][n] row-major. */
+typedef struct {
+    float Q[64];
+} mppi_linear_cost_t;
+
+typedef struct {
+    uint32_t struct_size;            /* sizeof(mppi_cost_t) */
+    float penalty;                   /* S~_k of a rollout whose cost is not finite; e.g. 1e30 */
+    union {
+        mppi_cartpole_cost_t cartpole;
+        mppi_racecar_cost_t racecar;
+        mppi_quadrotor_cost_t quadrotor;
+        mppi_linear_cost_t linear;
+    } p;
+} mppi_cost_t;
+
+/* ---------------------------------------------------------------- sharding across GPUs */
+
+/* K is split into world contiguous shards; rank r owns global samples
+ * [r*K/world, (r+1)*K/world).  Noise counters use the GLOBAL sample index, so the union of
+ * the shards' noise equals the single-GPU noise bit for bit.  The two
+ * cross-rank reductions (MIN of the cost key, SUM of [eta, A]) are done by the caller
+ * between the split-phase calls below (e.g. NCCL allreduce via torch.distributed). */
+typedef struct {
+    int32_t rank;
+    int32_t world;
+} mppi_dist_t;
+
+typedef struct mppi_ctx mppi_ctx;
+
+typedef struct {
+    int32_t n, m, T;
+    int32_t plant;
+    int64_t K;                       /* global sample count */
+    int64_t K_loc;                   /* samples of this rank */
+    int64_t k_offset;                /* first global sample of this rank */
+    int32_t n_chunks;                /* K-chunks of the weighted-noise reduction (partials rows) */
+    int32_t reserved;
+    size_t workspace_bytes;          /* device memory owned by the context */
+} mppi_info_t;
+
+/* Host-readable summary of the last completed step (see mppi_get_stats). */
+typedef struct {
+    int64_t k_star;                  /* global index of the minimum-cost sample (ties: smallest k) */
+    float s_min;                     /* S_min = S~_{k*} */
+    float eta;                       /* normaliser sum_k exp(-(S~_k - S_min)/lambda) (global after apply) */
+} mppi_stats_t;
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* mppi_create — Alg. 1 "Given" block.
+ *   dynamics, cost : HOST structs, copied (obstacles too).  cost->penalty must be finite.
+ *   K              : global number of samples, >= 1; K_loc = K/world must be an integer
+ *                    multiple of 4 (16-byte aligned noise rows).
+ *   T              : horizon steps, 1..4096.
+ *   dt             : Euler step > 0.
+ *   lambda         : temperature > 0.
+ *   nu             : exploration variance scale >= 1 (PAPER.md:308; Gamma invertible, :197).
+ *   m              : control dimension; must equal the plant's (1, 2, 4, or 1..4 for LINEAR).
+ *   Sigma          : HOST fp64 [m][m], the natural covariance of delta-u (PAPER.md:312:
+ *                    du = eps/(sqrt(rho) sqrt(dt)) -> Sigma = I/(rho dt) in the special case).
+ *                    The sampling covariance is nu*Sigma.  Factored in fp64 (Cholesky), used as fp32.
+ *   R              : HOST fp64 [m][m] SPD control-cost matrix.
+ *   dist           : HOST, NULL for a single GPU.
+ *   cuda_stream    : cudaStream_t (NULL = legacy default stream) on the current device; all
+ *                    work of this context is enqueued on it.
+ *   out            : receives the context.
+ * Synchronous.  Allocates the workspace (noise [T][K_loc][m], costs, reduction partials).
+ * Errors: INVALID_ARG, NOT_SPD, OOM, CUDA. */
+mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* cost, int64_t K,
+                          int32_t T, float dt, float lambda, float nu, int32_t m,
+                          const double* Sigma, const double* R, const mppi_dist_t* dist,
+                          void* cuda_stream, mppi_ctx** out);
+
+/* Frees the context after synchronising its stream.  NULL is a no-op. */
+void mppi_destroy(mppi_ctx* ctx);
+
+mppi_status_t mppi_info(const mppi_ctx* ctx, mppi_info_t* out /* HOST */);
+
+/* Changes the stream later calls enqueue on (e.g. torch's current stream). */
+mppi_status_t mppi_set_stream(mppi_ctx* ctx, void* cuda_stream);
+
+/* ---------------------------------------------------------------- the step */
+
+/* mppi_optimize — one full MPPI step, world == 1 only (else UNSUPPORTED):
+ *   noise -> rollout -> min -> weights + weighted noise sum -> U update.
+ *   x0    : HOST float [n], the current state x_{t0}; read before return (passed by value).
+ *   U     : DEVICE float [T][m], the nominal control sequence, updated in place.
+ *   seed, step : Philox key and counter words; eps[t][k][j] = j-th normal of
+ *           Philox4x32-10(ctr = (k, t, step_lo, step_hi), key = (seed_lo, seed_hi)) transformed
+ *           by the fixed fp32 Box-Muller sequence of SURVEY.md Appendix B.
+ *   noise : NULL -> generate eps as above into the context; otherwise DEVICE float [T][K][m]
+ *           of N(0,1) samples supplied by the caller (seed/step ignored), read-only.
+ * Errors: INVALID_ARG (NULL U, non-finite x0), UNSUPPORTED (world > 1), CUDA. */
+mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed,
+                            uint64_t step, const float* noise);
+
+/* mppi_optimize_host — the same step end to end from HOST buffers: copies x0 and U in,
+ * runs mppi_optimize on the context's device copy of U, copies the updated U back.
+ * SYNCHRONOUS (returns after U is in host memory).  U: HOST float [T][m] in/out. */
+mppi_status_t mppi_optimize_host(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed,
+                                 uint64_t step);
+
+/* ---------------------------------------------------------------- split phase (multi-GPU) */
+
+/* mppi_rollout_costs — noise (unless supplied) and rollouts of this rank's K_loc samples.
+ *   costs   : DEVICE float [K_loc] or NULL; receives S~_k (penalty where non-finite).
+ *   min_key : DEVICE int64 [1] or NULL; receives this rank's minimum key
+ *             key = (int64)ord32(S_min) << 32 | k_global, ord32 the order-preserving signed
+ *             map of the fp32 bits (b >= 0 ? b : b ^ 0x7fffffff).  The smallest key is the
+ *             smallest cost, ties to the smallest global k; combine ranks with a signed MIN.
+ * The context keeps its own copy of the costs and the key for mppi_accumulate. */
+mppi_status_t mppi_rollout_costs(mppi_ctx* ctx, const float* x0, const float* U, uint64_t seed,
+                                 uint64_t step, const float* noise, float* costs,
+                                 int64_t* min_key);
+
+/* mppi_accumulate — weights and weighted noise sum over this rank's samples.
+ *   global_min_key : DEVICE int64 [1], the MIN over ranks of the keys (NULL: this rank's key).
+ *   buf            : DEVICE float [1 + T*m] receiving [eta_r, A_r[0][0..m), ..., A_r[T-1][..]]
+ *                    with eta_r = sum_k w_k and A_r[t][j] = sum_k w_k eps[t][k][j] over this
+ *                    rank's k in a fixed order (deterministic).  SUM it over ranks, then apply. */
+mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, float* buf);
+
+/* mppi_apply — U_t += sqrt(nu) L A[t] / eta with [eta, A] = buf (DEVICE, read-only),
+ * U DEVICE [T][m] in place.  Per entry: d_i = sum_{j<=i} fl(sL[i][j]*A[t][j]) accumulated in
+ * order j = 0..i, U[t][i] = fl(U[t][i] + fl(d_i / eta)). */
+mppi_status_t mppi_apply(mppi_ctx* ctx, float* U, const float* buf);
+
+/* ---------------------------------------------------------------- helpers around the step */
+
+/* mppi_shift — Alg. 1: U_i = U_{i+1}, U_{T-1} = u_init.
+ *   U DEVICE [T][m] in place; u_init HOST float [m]. */
+mppi_status_t mppi_shift(mppi_ctx* ctx, float* U, const float* u_init);
+
+/* mppi_noise — writes this rank's eps [T][K_loc][m] for (seed, step) into `out` (DEVICE). */
+mppi_status_t mppi_noise(mppi_ctx* ctx, uint64_t seed, uint64_t step, float* out);
+
+/* mppi_plant_step — advances the plant one Euler step on the HOST with the same fp32 plant
+ * code the rollout kernel runs (environment simulation for closed-loop MPC, Alg. 1 :377).
+ *   x HOST float [n] in/out; u HOST float [m]; crashed HOST int32 in/out (quadrotor C flag,
+ *   may be NULL); q_out HOST float or NULL receives q(x').  Synchronous; touches no device. */
+mppi_status_t mppi_plant_step(mppi_ctx* ctx, float* x, const float* u, int32_t* crashed,
+                              float* q_out);
+
+/* mppi_get_stats — SYNCHRONOUS: waits for the stream, then reads the last step's k*, S_min
+ * and eta (eta is this rank's local sum unless mppi_apply ran with a summed buffer). */
+mppi_status_t mppi_get_stats(mppi_ctx* ctx, mppi_stats_t* out /* HOST */);
+
+/* Number of kernels the last mppi_optimize / split-phase call enqueued (for launch accounting). */
+int32_t mppi_last_launch_count(const mppi_ctx* ctx);
+
+/* ---------------------------------------------------------------- per-kernel device time */
+
+typedef enum {
+    MPPI_KERNEL_NOISE = 0,     /* K1 noise_kernel */
+    MPPI_KERNEL_ROLLOUT = 1,   /* K2 rollout_kernel */
+    MPPI_KERNEL_WSUM = 2,      /* K3 wsum_kernel (weights + weighted noise sum) */
+    MPPI_KERNEL_FINALIZE = 3,  /* K4 finalize_kernel (partials -> [eta, A] -> U) */
+    MPPI_KERNEL_SHIFT = 4,     /* K5 shift_kernel */
+    MPPI_KERNEL_KINDS = 5
+} mppi_kernel_kind_t;
+
+typedef struct {
+    double total_ms[MPPI_KERNEL_KINDS];  /* summed CUDA-event time of the launches of each kind */
+    int64_t launches[MPPI_KERNEL_KINDS];
+} mppi_kernel_times_t;
+
+/* mppi_profile_enable — while enabled, every kernel launch of this context is bracketed by two
+ * CUDA events recorded on the context stream (the stream the kernel runs on). */
+mppi_status_t mppi_profile_enable(mppi_ctx* ctx, int32_t enable);
+
+/* mppi_profile_read — SYNCHRONOUS: waits for the stream, returns the accumulated per-kind times
+ * since the last read (or enable), and resets them.  out: HOST. */
+mppi_status_t mppi_profile_read(mppi_ctx* ctx, mppi_kernel_times_t* out);
+
+const char* mppi_last_error(void);           /* thread-local, never NULL */
+const char* mppi_status_string(mppi_status_t s);
+int32_t mppi_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPPI_B200_H */

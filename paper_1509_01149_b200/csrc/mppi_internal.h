@@ -1,0 +1,95 @@
+// mppi_internal.h — context layout and kernel launchers shared by mppi_kernels.cu and
+// mppi_runtime.cu (internal; the public boundary is include/mppi.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "mppi.h"
+#include "noise.cuh"
+#include "plants.cuh"
+
+namespace mppi {
+
+constexpr int kRolloutThreads = 128;
+constexpr int kWsumThreads = 256;
+constexpr int kWsumTT = 8;  // timesteps per weighted-noise tile (register accumulators = 8 * m)
+
+union PlantParamsU {
+    CartpoleParams cartpole;
+    RacecarParams racecar;
+    QuadrotorParams quadrotor;
+    LinearParams linear;
+};
+
+// Device-side per-step results readable by mppi_get_stats.
+struct DeviceStats {
+    long long min_key;
+    float eta;
+    float pad;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int plant = 0, n = 0, m = 0, T = 0;
+    int64_t K = 0, K_loc = 0, k_offset = 0;
+    int rank = 0, world = 1;
+    float dt = 0, lambda = 0, nu = 1, c1 = 0, penalty = 1e30f;
+    bool diag = true;               // L and R both diagonal -> diagonal fast path
+    float sL[16] = {0};             // sqrt(nu) * chol(Sigma), fp32, row-major m x m
+    float R[16] = {0};              // control cost, fp32
+    PlantParamsU params;            // pre-digested plant/cost parameters
+    std::vector<float4> obs_host;   // negated obstacle pairs (host copy, for mppi_plant_step)
+    int n_obs_pairs = 0;
+    // device workspace
+    float4* d_obs = nullptr;
+    float* d_eps = nullptr;         // [T][K_loc][m]
+    float* d_costs = nullptr;       // [K_loc]
+    long long* d_key_init = nullptr;  // constant INT64_MAX (reset source)
+    float* d_part = nullptr;        // [n_chunks][T*m]
+    float* d_eta_part = nullptr;    // [n_chunks]
+    DeviceStats* d_stats = nullptr;
+    float* d_U = nullptr;           // [T][m] for mppi_optimize_host
+    float* h_U_pinned = nullptr;    // pinned staging for mppi_optimize_host
+    int n_chunks = 1;
+    int64_t cols_per_chunk = 0;     // float4 columns of a noise row per chunk
+    size_t workspace_bytes = 0;
+    int last_launches = 0;
+    const float* last_eps = nullptr;  // noise read by the last rollout (ctx or caller buffer)
+    // per-kernel CUDA-event timing (mppi_profile_enable)
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;                       // free events
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
+    double prof_ms[MPPI_KERNEL_KINDS] = {0};
+    int64_t prof_n[MPPI_KERNEL_KINDS] = {0};
+};
+
+// Brackets one kernel launch with CUDA events when profiling is on.
+struct ProfScope {
+    Ctx& c;
+    int kind;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(Ctx& c_, int kind_);
+    ~ProfScope();
+};
+
+// launchers (mppi_kernels.cu); each returns the CUDA error of the launch
+cudaError_t launch_noise(Ctx& c, uint64_t seed, uint64_t step, float* out, bool reset_key);
+cudaError_t launch_rollout(Ctx& c, const float* x0, const float* U, const float* eps,
+                           float* costs_out);
+cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key);
+cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* U);
+cudaError_t launch_shift(Ctx& c, float* U, const float* u_init);
+
+// host plant step (mppi_runtime.cu uses it for mppi_plant_step)
+float host_plant_step(const Ctx& c, float* x, const float* u, int32_t* crashed);
+
+}  // namespace mppi
+
+struct mppi_ctx {
+    mppi::Ctx c;
+};

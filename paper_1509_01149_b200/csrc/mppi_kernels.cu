@@ -1,0 +1,568 @@
+// mppi_kernels.cu — the sm_100a kernels of one MPPI step (Alg. 1, :356-368).
+//
+//   K1 noise_kernel     eps[t][k][0..m) from Philox4x32-10 + BM32        (HBM write / int ALU)
+//   K2 rollout_kernel   one sample per thread, state in registers, T Euler steps accumulating
+//                       S~_k = sum_t q~; block min -> atomicMin key
+//                                                                          (FP32 issue bound)
+//   K3 wsum_kernel      w_k = exp(-(S~_k - S_min)/lambda) and A[t][j] = sum_k w_k eps[t][k][j]:
+//                       the memory-bound K x (T m) GEMV, per-chunk partials  (HBM read bound)
+//   K4 finalize_kernel  fixed-order sum of partials, U_t += sqrt(nu) L A_t / eta
+//   K5 shift_kernel     U_i = U_{i+1}, U_{T-1} = u_init
+//
+// No float atomics anywhere: every reduction has a fixed order, so a step is bitwise
+// reproducible run to run.  The only atomic is an integer atomicMin on the
+// 64-bit (cost, k) key, which is order independent.
+#include <climits>
+
+#include "mppi_internal.h"
+
+namespace mppi {
+
+// ------------------------------------------------------------------------------ helpers
+template <int M>
+__device__ __forceinline__ void load_eps(const float* p, float* e) {
+    if constexpr (M == 4) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(p));
+        e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
+    } else if constexpr (M == 2) {
+        const float2 v = __ldcs(reinterpret_cast<const float2*>(p));
+        e[0] = v.x; e[1] = v.y;
+    } else {
+        e[0] = __ldcs(p);
+    }
+}
+
+template <int M>
+__device__ __forceinline__ void store_eps(float* p, const float* z) {
+    if constexpr (M == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(z[0], z[1], z[2], z[3]);
+    } else if constexpr (M == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(z[0], z[1]);
+    } else {
+        *p = z[0];
+    }
+}
+
+// Order-preserving signed map of fp32 bits, then (cost, k) packed so that signed int64 MIN
+// picks the smallest cost and, among ties, the smallest global k.
+__device__ __forceinline__ long long cost_key(float s, unsigned k) {
+    int b = __float_as_int(s);
+    b = b >= 0 ? b : (b ^ 0x7fffffff);
+    return (long long)(((unsigned long long)(unsigned)b << 32) | (unsigned long long)k);
+}
+
+__device__ __forceinline__ float key_cost(long long key) {
+    int b = (int)(key >> 32);
+    b = b >= 0 ? b : (b ^ 0x7fffffff);
+    return __int_as_float(b);
+}
+
+__device__ __forceinline__ long long warp_min_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ------------------------------------------------------------------------------ K1 noise
+// One thread per (t, k): grid (ceil(K_loc/256), T).  Block (0,0) also resets the min key for the
+// rollout that follows on the same stream.
+template <int M>
+__global__ void __launch_bounds__(256) noise_kernel(float* __restrict__ eps, int K_loc,
+                                                    unsigned k_offset, unsigned step_lo,
+                                                    unsigned step_hi, const PhiloxKeys keys,
+                                                    long long* key_reset) {
+    const int k = blockIdx.x * 256 + threadIdx.x;
+    const unsigned t = blockIdx.y;
+    if (key_reset && k == 0 && t == 0) *key_reset = LLONG_MAX;
+    if (k >= K_loc) return;
+    const uint4 w = philox4x32_10_dev(k_offset + (unsigned)k, t, step_lo, step_hi, keys);
+    float z[M];
+    bm32_normals<M>(w, z);
+    store_eps<M>(eps + ((size_t)t * K_loc + k) * M, z);
+}
+
+// ------------------------------------------------------------------------------ K2 rollout
+template <class PP>
+struct RolloutArgs {
+    const float* eps;       // [T][K_loc][M]
+    const float* U;         // [T][M]
+    float* costs;           // [K_loc] (context copy)
+    float* costs_out;       // [K_loc] caller copy or nullptr
+    long long* min_key;     // reset to INT64_MAX before launch
+    const float4* obs;      // negated obstacle pairs
+    int n_obs_pairs;
+    int T;
+    int K_loc;
+    unsigned k_offset;
+    float dt, c1, penalty;
+    float sL[16];           // sqrt(nu) chol(Sigma)
+    float R[16];
+    float x0[16];
+    PP P;
+};
+
+template <class Plant, bool DIAG>
+__global__ void __launch_bounds__(kRolloutThreads)
+    rollout_kernel(const RolloutArgs<typename Plant::Params> a) {
+    constexpr int M = Plant::M;
+    extern __shared__ float4 smem4[];
+    float4* sObs = smem4;
+    float* sU = reinterpret_cast<float*>(smem4 + a.n_obs_pairs);  // U_t        [T][M]
+    float* sRU = sU + a.T * M;                                     // R U_t      [T][M]
+    float* sK = sRU + a.T * M;                                     // U_t'R U_t/2 [T]
+    const int tid = threadIdx.x;
+    for (int i = tid; i < a.n_obs_pairs; i += blockDim.x) sObs[i] = a.obs[i];
+    for (int t = tid; t < a.T; t += blockDim.x) {
+        float u[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) u[i] = a.U[t * M + i];
+        float kk = 0.0f;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            float s = 0.0f;
+#pragma unroll
+            for (int j = 0; j < M; ++j) s = fmaf(a.R[i * M + j], u[j], s);
+            sU[t * M + i] = u[i];
+            sRU[t * M + i] = s;
+            kk = fmaf(u[i], s, kk);
+        }
+        sK[t] = 0.5f * kk;
+    }
+    __syncthreads();
+
+    const int k = blockIdx.x * blockDim.x + tid;
+    long long key = LLONG_MAX;
+    if (k < a.K_loc) {
+        Plant st;
+        st.load(a.x0, 0);
+        const ObstacleView ob{sObs, a.n_obs_pairs};
+        const size_t row = (size_t)a.K_loc * M;
+        const float* ep = a.eps + (size_t)k * M;
+        float e[M];
+        load_eps<M>(ep, e);
+        float S = 0.0f;
+        for (int t = 0; t < a.T; ++t) {
+            float en[M];  // prefetch eps of step t+1 (clamped: the last prefetch re-reads row T-1)
+            load_eps<M>(ep + (size_t)min(t + 1, a.T - 1) * row, en);
+            float du[M], v[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                if (DIAG) {
+                    du[i] = a.sL[i * M + i] * e[i];
+                } else {
+                    float s = 0.0f;
+#pragma unroll
+                    for (int j = 0; j <= i; ++j) s = fmaf(a.sL[i * M + j], e[j], s);
+                    du[i] = s;
+                }
+                v[i] = sU[t * M + i] + du[i];               // u_i + du_{i,k}
+            }
+            const float q = st.step(v, a.dt, a.P, ob);      // x_{t+1}, q(x_{t+1})
+            float duRdu = 0.0f, uRdu = 0.0f;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                if (DIAG) {
+                    duRdu = fmaf(a.R[i * M + i] * du[i], du[i], duRdu);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < M; ++j) duRdu = fmaf(du[i] * a.R[i * M + j], du[j], duRdu);
+                }
+                uRdu = fmaf(sRU[t * M + i], du[i], uRdu);
+            }
+            // q~ = q + (1 - 1/nu)/2 du'R du + u'R du + u'R u / 2
+            S += q + fmaf(a.c1, duRdu, uRdu + sK[t]);
+#pragma unroll
+            for (int i = 0; i < M; ++i) e[i] = en[i];
+        }
+        if (!isfinite(S)) S = a.penalty;
+        a.costs[k] = S;
+        if (a.costs_out) a.costs_out[k] = S;
+        key = cost_key(S, a.k_offset + (unsigned)k);
+    }
+    key = warp_min_ll(key);
+    __shared__ long long wmin[kRolloutThreads / 32];
+    if ((tid & 31) == 0) wmin[tid >> 5] = key;
+    __syncthreads();
+    if (tid < 32) {
+        long long v = tid < (int)(blockDim.x >> 5) ? wmin[tid] : LLONG_MAX;
+        v = warp_min_ll(v);
+        if (tid == 0 && v != LLONG_MAX) atomicMin(a.min_key, v);
+    }
+}
+
+// ------------------------------------------------------------------------------ K3 weights + GEMV
+struct WsumArgs {
+    const float* eps;           // [T][K_loc][M] viewed as [T][ncols] float4
+    const float* costs;         // [K_loc]
+    const long long* key;       // global min key
+    float* part;                // [n_chunks][T][M]
+    float* eta_part;            // [n_chunks]
+    int T;
+    long long ncols;            // K_loc * M / 4
+    long long cols_per_chunk;
+    float lambda;
+};
+
+// grid (n_chunks, ceil(T / TT)); each thread owns float4 columns (4/M samples each) of its
+// chunk and accumulates TT x 4 partial sums in registers over the chunk, with TT independent
+// 16-byte loads in flight per iteration.  w_k is computed once per sample per t-tile.
+template <int M>
+__global__ void __launch_bounds__(kWsumThreads) wsum_kernel(const WsumArgs a) {
+    constexpr int SPC = 4 / M;  // samples per float4 column
+    constexpr int TT = kWsumTT;
+    const int chunk = blockIdx.x;
+    const int t0 = blockIdx.y * TT;
+    const int nt = min(TT, a.T - t0);
+    const float smin = key_cost(*a.key);
+    const long long c_begin = (long long)chunk * a.cols_per_chunk;
+    const long long c_end = min(a.ncols, c_begin + a.cols_per_chunk);
+    const float4* __restrict__ eps4 = reinterpret_cast<const float4*>(a.eps);
+    const bool do_eta = blockIdx.y == 0;
+    float acc[TT][4];
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[tt][c] = 0.0f;
+    float eta = 0.0f;
+    for (long long col = c_begin + threadIdx.x; col < c_end; col += kWsumThreads) {
+        float cs[SPC];
+        if constexpr (SPC == 4) {
+            const float4 c = __ldg(reinterpret_cast<const float4*>(a.costs) + col);
+            cs[0] = c.x; cs[1] = c.y; cs[2] = c.z; cs[3] = c.w;
+        } else if constexpr (SPC == 2) {
+            const float2 c = __ldg(reinterpret_cast<const float2*>(a.costs) + col);
+            cs[0] = c.x; cs[1] = c.y;
+        } else {
+            cs[0] = __ldg(a.costs + col);
+        }
+        float w[SPC];
+#pragma unroll
+        for (int s = 0; s < SPC; ++s) {
+            w[s] = expf(-__fdiv_rn(cs[s] - smin, a.lambda));  // PAPER.md:320 (min-shifted)
+            if (do_eta) eta += w[s];
+        }
+        float4 v[TT];
+#pragma unroll
+        for (int tt = 0; tt < TT; ++tt)
+            if (tt < nt) v[tt] = __ldcs(eps4 + (size_t)(t0 + tt) * a.ncols + col);
+#pragma unroll
+        for (int tt = 0; tt < TT; ++tt) {
+            if (tt < nt) {
+                acc[tt][0] = fmaf(w[0 / M], v[tt].x, acc[tt][0]);
+                acc[tt][1] = fmaf(w[1 / M], v[tt].y, acc[tt][1]);
+                acc[tt][2] = fmaf(w[2 / M], v[tt].z, acc[tt][2]);
+                acc[tt][3] = fmaf(w[3 / M], v[tt].w, acc[tt][3]);
+            }
+        }
+    }
+    // fold the 4 lanes of a column onto the M control components, then block-reduce
+    __shared__ float red[kWsumThreads / 32][TT * M + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt) {
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            float f = 0.0f;
+#pragma unroll
+            for (int s = 0; s < SPC; ++s) f += acc[tt][s * M + j];
+            f = warp_sum(f);
+            if (lane == 0) red[warp][tt * M + j] = f;
+        }
+    }
+    eta = warp_sum(eta);
+    if (lane == 0) red[warp][TT * M] = eta;
+    __syncthreads();
+    if (threadIdx.x < TT * M + 1) {
+        float s = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kWsumThreads / 32; ++w) s += red[w][threadIdx.x];
+        if (threadIdx.x < TT * M) {
+            const int tt = threadIdx.x / M, j = threadIdx.x % M;
+            if (tt < nt) a.part[((size_t)chunk * a.T + t0 + tt) * M + j] = s;
+        } else if (do_eta) {
+            a.eta_part[chunk] = s;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------ K4 finalize / apply
+struct FinalizeArgs {
+    const float* part;
+    const float* eta_part;
+    int n_chunks;
+    const float* buf_in;   // [1 + T*M] = [eta, A] (already summed over ranks) or nullptr
+    float* buf_out;        // [1 + T*M] or nullptr
+    float* U;              // [T][M] updated in place, or nullptr
+    DeviceStats* stats;
+    int T, M;
+    float sL[16];
+};
+
+__global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeArgs a) {
+    extern __shared__ float sA[];  // [1 + T*M]: eta, A
+    const int TM = a.T * a.M;
+    if (a.buf_in) {
+        for (int o = threadIdx.x; o < TM + 1; o += blockDim.x) sA[o] = a.buf_in[o];
+    } else {
+        for (int o = threadIdx.x; o < TM; o += blockDim.x) {
+            float s = 0.0f;
+            for (int c = 0; c < a.n_chunks; ++c) s += a.part[(size_t)c * TM + o];  // chunk order
+            sA[1 + o] = s;
+        }
+        if (threadIdx.x == 0) {
+            float e = 0.0f;
+            for (int c = 0; c < a.n_chunks; ++c) e += a.eta_part[c];
+            sA[0] = e;
+        }
+    }
+    __syncthreads();
+    if (a.buf_out)
+        for (int o = threadIdx.x; o < TM + 1; o += blockDim.x) a.buf_out[o] = sA[o];
+    if (a.stats && threadIdx.x == 0) a.stats->eta = sA[0];
+    if (a.U) {
+        const float eta = sA[0];
+        for (int o = threadIdx.x; o < TM; o += blockDim.x) {
+            const int t = o / a.M, i = o % a.M;
+            float d = 0.0f;  // d_i = sum_{j<=i} sL[i][j] A[t][j], explicit rounding order
+            for (int j = 0; j <= i; ++j) d = __fadd_rn(d, __fmul_rn(a.sL[i * a.M + j], sA[1 + t * a.M + j]));
+            a.U[o] = __fadd_rn(a.U[o], __fdiv_rn(d, eta));   // U_t += sum w du / eta
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------ K5 shift
+__global__ void __launch_bounds__(1024) shift_kernel(float* U, int T, int M, float4 u_init) {
+    extern __shared__ float sU[];
+    const int TM = T * M;
+    for (int o = threadIdx.x; o < TM; o += blockDim.x) sU[o] = U[o];
+    __syncthreads();
+    for (int o = threadIdx.x; o < TM; o += blockDim.x) {
+        float v;
+        if (o < TM - M) {
+            v = sU[o + M];
+        } else {
+            const int i = o - (TM - M);
+            v = i == 0 ? u_init.x : (i == 1 ? u_init.y : (i == 2 ? u_init.z : u_init.w));
+        }
+        U[o] = v;
+    }
+}
+
+// ============================================================================== launchers
+static cudaEvent_t take_event(Ctx& c) {
+    if (!c.ev_pool.empty()) {
+        cudaEvent_t e = c.ev_pool.back();
+        c.ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+ProfScope::ProfScope(Ctx& c_, int kind_) : c(c_), kind(kind_) {
+    if (!c.prof) return;
+    a = take_event(c);
+    b = take_event(c);
+    cudaEventRecord(a, c.stream);
+}
+
+ProfScope::~ProfScope() {
+    if (!c.prof || !a) return;
+    cudaEventRecord(b, c.stream);
+    c.ev_pending.push_back(std::make_pair(kind, std::make_pair(a, b)));
+}
+
+static PhiloxKeys philox_key_schedule(uint64_t seed) {
+    PhiloxKeys K;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        K.k0[r] = k0;
+        K.k1[r] = k1;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return K;
+}
+
+cudaError_t launch_noise(Ctx& c, uint64_t seed, uint64_t step, float* out, bool reset_key) {
+    const PhiloxKeys keys = philox_key_schedule(seed);
+    const dim3 grid((unsigned)((c.K_loc + 255) / 256), (unsigned)c.T);
+    ProfScope prof(c, MPPI_KERNEL_NOISE);
+    long long* kr = reset_key ? reinterpret_cast<long long*>(&c.d_stats->min_key) : nullptr;
+    const unsigned ko = (unsigned)c.k_offset, slo = (unsigned)step, shi = (unsigned)(step >> 32);
+    switch (c.m) {
+        case 1: noise_kernel<1><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, ko, slo, shi, keys, kr); break;
+        case 2: noise_kernel<2><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, ko, slo, shi, keys, kr); break;
+        case 4: noise_kernel<4><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, ko, slo, shi, keys, kr); break;
+        default: return cudaErrorInvalidValue;
+    }
+    c.last_launches++;
+    return cudaGetLastError();
+}
+
+template <class Plant, bool DIAG>
+static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, const float* x0,
+                                    const float* U, const float* eps, float* costs_out) {
+    RolloutArgs<typename Plant::Params> a;
+    a.eps = eps;
+    a.U = U;
+    a.costs = c.d_costs;
+    a.costs_out = costs_out;
+    a.min_key = &c.d_stats->min_key;
+    a.obs = c.d_obs;
+    a.n_obs_pairs = c.n_obs_pairs;
+    a.T = c.T;
+    a.K_loc = (int)c.K_loc;
+    a.k_offset = (unsigned)c.k_offset;
+    a.dt = c.dt;
+    a.c1 = c.c1;
+    a.penalty = c.penalty;
+    for (int i = 0; i < 16; ++i) { a.sL[i] = c.sL[i]; a.R[i] = c.R[i]; a.x0[i] = 0.0f; }
+    for (int i = 0; i < c.n && i < 16; ++i) a.x0[i] = x0[i];
+    a.P = P;
+    const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) +
+                        (size_t)(2 * c.T * Plant::M + c.T) * sizeof(float);
+    auto kern = rollout_kernel<Plant, DIAG>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const unsigned grid = (unsigned)((c.K_loc + kRolloutThreads - 1) / kRolloutThreads);
+    ProfScope prof(c, MPPI_KERNEL_ROLLOUT);
+    kern<<<grid, kRolloutThreads, smem, c.stream>>>(a);
+    c.last_launches++;
+    return cudaGetLastError();
+}
+
+template <class Plant>
+static cudaError_t launch_rollout_p(Ctx& c, const typename Plant::Params& P, const float* x0,
+                                    const float* U, const float* eps, float* costs_out) {
+    return c.diag ? launch_rollout_t<Plant, true>(c, P, x0, U, eps, costs_out)
+                  : launch_rollout_t<Plant, false>(c, P, x0, U, eps, costs_out);
+}
+
+cudaError_t launch_rollout(Ctx& c, const float* x0, const float* U, const float* eps,
+                           float* costs_out) {
+    switch (c.plant) {
+        case MPPI_PLANT_CARTPOLE:
+            return launch_rollout_p<Cartpole>(c, c.params.cartpole, x0, U, eps, costs_out);
+        case MPPI_PLANT_RACECAR:
+            return launch_rollout_p<Racecar>(c, c.params.racecar, x0, U, eps, costs_out);
+        case MPPI_PLANT_QUADROTOR:
+            return launch_rollout_p<Quadrotor>(c, c.params.quadrotor, x0, U, eps, costs_out);
+        case MPPI_PLANT_LINEAR: {
+            float xp[16] = {0};
+            for (int i = 0; i < c.n; ++i) xp[i] = x0[i];
+            if (c.m == 1) return launch_rollout_p<Linear<1>>(c, c.params.linear, xp, U, eps, costs_out);
+            if (c.m == 2) return launch_rollout_p<Linear<2>>(c, c.params.linear, xp, U, eps, costs_out);
+            if (c.m == 4) return launch_rollout_p<Linear<4>>(c, c.params.linear, xp, U, eps, costs_out);
+            return cudaErrorInvalidValue;
+        }
+        default:
+            return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key) {
+    WsumArgs a;
+    a.eps = eps;
+    a.costs = c.d_costs;
+    a.key = key;
+    a.part = c.d_part;
+    a.eta_part = c.d_eta_part;
+    a.T = c.T;
+    a.ncols = c.K_loc * c.m / 4;
+    a.cols_per_chunk = c.cols_per_chunk;
+    a.lambda = c.lambda;
+    const dim3 grid((unsigned)c.n_chunks, (unsigned)((c.T + kWsumTT - 1) / kWsumTT));
+    ProfScope prof(c, MPPI_KERNEL_WSUM);
+    switch (c.m) {
+        case 1: wsum_kernel<1><<<grid, kWsumThreads, 0, c.stream>>>(a); break;
+        case 2: wsum_kernel<2><<<grid, kWsumThreads, 0, c.stream>>>(a); break;
+        case 4: wsum_kernel<4><<<grid, kWsumThreads, 0, c.stream>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
+    c.last_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* U) {
+    FinalizeArgs a;
+    a.part = c.d_part;
+    a.eta_part = c.d_eta_part;
+    a.n_chunks = c.n_chunks;
+    a.buf_in = buf_in;
+    a.buf_out = buf_out;
+    a.U = U;
+    a.stats = c.d_stats;
+    a.T = c.T;
+    a.M = c.m;
+    for (int i = 0; i < 16; ++i) a.sL[i] = c.sL[i];
+    const size_t smem = (size_t)(c.T * c.m + 1) * sizeof(float);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int threads = c.T * c.m >= 1024 ? 1024 : ((c.T * c.m + 31) / 32) * 32;
+    ProfScope prof(c, MPPI_KERNEL_FINALIZE);
+    finalize_kernel<<<1, threads, smem, c.stream>>>(a);
+    c.last_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shift(Ctx& c, float* U, const float* u_init) {
+    float4 ui = make_float4(0, 0, 0, 0);
+    float* up = reinterpret_cast<float*>(&ui);
+    for (int i = 0; i < c.m; ++i) up[i] = u_init[i];
+    const size_t smem = (size_t)c.T * c.m * sizeof(float);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(shift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int threads = c.T * c.m >= 1024 ? 1024 : ((c.T * c.m + 31) / 32) * 32;
+    ProfScope prof(c, MPPI_KERNEL_SHIFT);
+    shift_kernel<<<1, threads, smem, c.stream>>>(U, c.T, c.m, ui);
+    c.last_launches++;
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ host plant step
+template <class Plant>
+static float host_step_t(const Ctx& c, const typename Plant::Params& P, float* x, const float* u,
+                         int32_t* crashed) {
+    Plant st;
+    float xin[16] = {0};
+    for (int i = 0; i < c.n && i < 16; ++i) xin[i] = x[i];
+    st.load(xin, crashed ? *crashed : 0);
+    const ObstacleView ob{c.obs_host.data(), c.n_obs_pairs};
+    const float q = st.step(u, c.dt, P, ob);
+    float xo[16] = {0};
+    st.store(xo);
+    for (int i = 0; i < c.n; ++i) x[i] = xo[i];
+    if (crashed) *crashed = st.crashed;
+    return q;
+}
+
+float host_plant_step(const Ctx& c, float* x, const float* u, int32_t* crashed) {
+    switch (c.plant) {
+        case MPPI_PLANT_CARTPOLE: return host_step_t<Cartpole>(c, c.params.cartpole, x, u, crashed);
+        case MPPI_PLANT_RACECAR: return host_step_t<Racecar>(c, c.params.racecar, x, u, crashed);
+        case MPPI_PLANT_QUADROTOR: return host_step_t<Quadrotor>(c, c.params.quadrotor, x, u, crashed);
+        default:
+            if (c.m == 1) return host_step_t<Linear<1>>(c, c.params.linear, x, u, crashed);
+            if (c.m == 2) return host_step_t<Linear<2>>(c, c.params.linear, x, u, crashed);
+            return host_step_t<Linear<4>>(c, c.params.linear, x, u, crashed);
+    }
+}
+
+}  // namespace mppi

@@ -1,0 +1,567 @@
+// mppi_runtime.cu — host runtime behind include/mppi.h: validation, fp64 Cholesky of Sigma,
+// parameter digestion, workspace sizing/allocation and the enqueue sequences of the step.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <new>
+#include <string>
+
+#include "mppi_internal.h"
+
+using namespace mppi;
+
+namespace {
+
+thread_local std::string g_err;
+
+mppi_status_t fail(mppi_status_t s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+mppi_status_t cuda_fail(cudaError_t e, const char* what) {
+    return fail(MPPI_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define MPPI_CUDA(call, what)                          \
+    do {                                               \
+        cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+bool is_fin(double v) { return std::isfinite(v); }
+
+// fp64 Cholesky A = L L^T (lower); false if A is not symmetric positive definite.
+bool cholesky64(const double* A, int m, double* L) {
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j)
+            if (!is_fin(A[i * m + j]) || fabs(A[i * m + j] - A[j * m + i]) > 1e-12 * (fabs(A[i * m + j]) + 1e-300))
+                return false;
+    for (int i = 0; i < m * m; ++i) L[i] = 0.0;
+    for (int j = 0; j < m; ++j) {
+        double d = A[j * m + j];
+        for (int k = 0; k < j; ++k) d -= L[j * m + k] * L[j * m + k];
+        if (!(d > 0.0)) return false;
+        L[j * m + j] = sqrt(d);
+        for (int i = j + 1; i < m; ++i) {
+            double s = A[i * m + j];
+            for (int k = 0; k < j; ++k) s -= L[i * m + k] * L[j * m + k];
+            L[i * m + j] = s / L[j * m + j];
+        }
+    }
+    return true;
+}
+
+int plant_state_dim(int plant) {
+    switch (plant) {
+        case MPPI_PLANT_CARTPOLE: return 4;
+        case MPPI_PLANT_RACECAR: return 6;
+        case MPPI_PLANT_QUADROTOR: return 16;
+        default: return 0;
+    }
+}
+int plant_control_dim(int plant) {
+    switch (plant) {
+        case MPPI_PLANT_CARTPOLE: return 1;
+        case MPPI_PLANT_RACECAR: return 2;
+        case MPPI_PLANT_QUADROTOR: return 4;
+        default: return 0;
+    }
+}
+
+bool all_finite(const float* p, int n) {
+    for (int i = 0; i < n; ++i)
+        if (!isfinite(p[i])) return false;
+    return true;
+}
+
+mppi_status_t digest_params(Ctx& c, const mppi_dynamics_t* d, const mppi_cost_t* q) {
+    memset(&c.params, 0, sizeof(c.params));
+    switch (c.plant) {
+        case MPPI_PLANT_CARTPOLE: {
+            const mppi_cartpole_dynamics_t& D = d->p.cartpole;
+            const mppi_cartpole_cost_t& Q = q->p.cartpole;
+            if (!(D.pole_length > 0) || !all_finite(&D.g, 3) || !all_finite(&Q.w_p, 4))
+                return fail(MPPI_ERR_INVALID_ARG, "cartpole: parameters must be finite, pole_length > 0");
+            CartpoleParams& P = c.params.cartpole;
+            P.g_over_l = (float)((double)D.g / D.pole_length);
+            P.inv_l = (float)(1.0 / D.pole_length);
+            P.kv = D.vel_gain;
+            P.w_p = Q.w_p; P.w_theta = Q.w_theta; P.w_thetadot = Q.w_thetadot; P.w_pdot = Q.w_pdot;
+            return MPPI_OK;
+        }
+        case MPPI_PLANT_RACECAR: {
+            const mppi_racecar_dynamics_t& D = d->p.racecar;
+            const mppi_racecar_cost_t& Q = q->p.racecar;
+            if (!all_finite(&D.mass, 15) || !all_finite(&Q.track_a, 5) || !(D.mass > 0) ||
+                !(D.Iz > 0) || !(D.lf + D.lr > 0) || !(D.v_min > 0) || !(Q.track_a > 0) ||
+                !(Q.track_b > 0) || D.throttle_min > D.throttle_max || D.steer_max < 0)
+                return fail(MPPI_ERR_INVALID_ARG, "racecar: invalid parameters");
+            RacecarParams& P = c.params.racecar;
+            const double L = (double)D.lf + D.lr;
+            P.inv_mass = (float)(1.0 / D.mass);
+            P.inv_Iz = (float)(1.0 / D.Iz);
+            P.lf = D.lf; P.lr = D.lr;
+            P.tire_B = D.tire_B; P.tire_C = D.tire_C;
+            P.Df = (float)((double)D.mu * D.mass * D.g * D.lr / L);
+            P.Dr = (float)((double)D.mu * D.mass * D.g * D.lf / L);
+            P.Cm = D.Cm; P.Cr = D.Cr; P.Cd = D.Cd; P.v_min = D.v_min;
+            P.steer_max = D.steer_max; P.throttle_min = D.throttle_min; P.throttle_max = D.throttle_max;
+            P.inv_a = (float)(1.0 / Q.track_a); P.inv_b = (float)(1.0 / Q.track_b);
+            P.w_track = Q.w_track; P.w_speed = Q.w_speed; P.v_ref = Q.v_ref;
+            return MPPI_OK;
+        }
+        case MPPI_PLANT_QUADROTOR: {
+            const mppi_quadrotor_dynamics_t& D = d->p.quadrotor;
+            const mppi_quadrotor_cost_t& Q = q->p.quadrotor;
+            if (!all_finite(&D.mass, 11) || !all_finite(Q.goal, 3) || !all_finite(&Q.w_xy, 9) ||
+                !(D.mass > 0) || !(D.Ixx > 0) || !(D.Iyy > 0) || !(D.Izz > 0) ||
+                !(D.cos_phi_min > 0) || !(Q.obs_length > 0) || Q.obstacle_radius < 0 ||
+                D.thrust_min > D.thrust_max)
+                return fail(MPPI_ERR_INVALID_ARG, "quadrotor: invalid parameters");
+            if (Q.n_obstacles < 0 || Q.n_obstacles > MPPI_MAX_OBSTACLES ||
+                (Q.n_obstacles > 0 && !Q.obstacles_xy))
+                return fail(MPPI_ERR_INVALID_ARG, "quadrotor: n_obstacles must be in [0, %d] with a host array",
+                            MPPI_MAX_OBSTACLES);
+            if (Q.n_obstacles > 0 && !all_finite(Q.obstacles_xy, 2 * Q.n_obstacles))
+                return fail(MPPI_ERR_INVALID_ARG, "quadrotor: obstacle centres must be finite");
+            QuadrotorParams& P = c.params.quadrotor;
+            P.inv_mass = (float)(1.0 / D.mass);
+            P.arm = D.arm;
+            P.inv_Ixx = (float)(1.0 / D.Ixx); P.inv_Iyy = (float)(1.0 / D.Iyy); P.inv_Izz = (float)(1.0 / D.Izz);
+            P.gyro_x = (float)((double)D.Izz - D.Iyy);
+            P.gyro_y = (float)((double)D.Ixx - D.Izz);
+            P.gyro_z = (float)((double)D.Iyy - D.Ixx);
+            P.yaw_coeff = D.yaw_coeff; P.motor_gain = D.motor_gain; P.g = D.g;
+            P.thrust_min = D.thrust_min; P.thrust_max = D.thrust_max; P.cos_phi_min = D.cos_phi_min;
+            P.gx = Q.goal[0]; P.gy = Q.goal[1]; P.gz = Q.goal[2];
+            P.w_xy = Q.w_xy; P.w_z = Q.w_z; P.w_yaw = Q.w_yaw; P.w_vel = Q.w_vel;
+            P.w_obs = Q.w_obs; P.inv_obs_length = (float)(1.0 / Q.obs_length); P.w_crash = Q.w_crash;
+            P.ground_z = Q.ground_z; P.radius = Q.obstacle_radius;
+            const int n = Q.n_obstacles;
+            c.n_obs_pairs = (n + 1) / 2;
+            c.obs_host.assign(c.n_obs_pairs, make_float4(-1e15f, -1e15f, -1e15f, -1e15f));
+            for (int j = 0; j < n; ++j) {
+                float4& p = c.obs_host[j / 2];
+                if (j % 2 == 0) { p.x = -Q.obstacles_xy[2 * j]; p.z = -Q.obstacles_xy[2 * j + 1]; }
+                else            { p.y = -Q.obstacles_xy[2 * j]; p.w = -Q.obstacles_xy[2 * j + 1]; }
+            }
+            return MPPI_OK;
+        }
+        case MPPI_PLANT_LINEAR: {
+            const mppi_linear_dynamics_t& D = d->p.linear;
+            const int n = D.n, m = c.m;
+            if (n < 1 || n > 8) return fail(MPPI_ERR_INVALID_ARG, "linear: n must be in 1..8");
+            if (!all_finite(D.A, n * n) || !all_finite(D.B, n * m) || !all_finite(q->p.linear.Q, n * n))
+                return fail(MPPI_ERR_INVALID_ARG, "linear: A, B, Q must be finite");
+            LinearParams& P = c.params.linear;
+            P.n = n;
+            P.m = m;
+            for (int i = 0; i < n; ++i) {
+                for (int j = 0; j < n; ++j) {
+                    P.A[i * 8 + j] = D.A[i * n + j];
+                    P.Q[i * 8 + j] = q->p.linear.Q[i * n + j];
+                }
+                for (int j = 0; j < m; ++j) P.B[i * 4 + j] = D.B[i * m + j];
+            }
+            c.n = n;
+            return MPPI_OK;
+        }
+        default:
+            return fail(MPPI_ERR_INVALID_ARG, "unknown plant %d", c.plant);
+    }
+}
+
+void free_ctx(Ctx& c) {
+    for (auto& p : c.ev_pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
+    for (auto e : c.ev_pool) cudaEventDestroy(e);
+    c.ev_pending.clear();
+    c.ev_pool.clear();
+    cudaFree(c.d_obs);
+    cudaFree(c.d_eps);
+    cudaFree(c.d_costs);
+    cudaFree(c.d_key_init);
+    cudaFree(c.d_part);
+    cudaFree(c.d_eta_part);
+    cudaFree(c.d_stats);
+    cudaFree(c.d_U);
+    if (c.h_U_pinned) cudaFreeHost(c.h_U_pinned);
+}
+
+template <class T>
+mppi_status_t dalloc(Ctx& c, T** p, size_t count, const char* what) {
+    const size_t bytes = count * sizeof(T);
+    cudaError_t e = cudaMalloc((void**)p, bytes > 0 ? bytes : 16);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return fail(MPPI_ERR_OOM, "cudaMalloc(%zu bytes) for %s failed", bytes, what);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    c.workspace_bytes += bytes;
+    return MPPI_OK;
+}
+
+mppi_status_t check_ctx(const mppi_ctx* ctx) {
+    if (!ctx) return fail(MPPI_ERR_INVALID_ARG, "ctx is NULL");
+    return MPPI_OK;
+}
+
+// Surface asynchronous faults of earlier work before enqueuing more.
+mppi_status_t sticky_check(Ctx& c) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "earlier CUDA error");
+    e = cudaStreamQuery(c.stream);
+    if (e != cudaSuccess && e != cudaErrorNotReady) return cuda_fail(e, "stream fault");
+    return MPPI_OK;
+}
+
+mppi_status_t do_rollout(Ctx& c, const float* x0, const float* U, uint64_t seed, uint64_t step,
+                         const float* noise, float* costs_out, const float** eps_used) {
+    if (!x0 || !U) return fail(MPPI_ERR_INVALID_ARG, "x0 and U must be non-NULL");
+    if (!all_finite(x0, c.n)) return fail(MPPI_ERR_INVALID_ARG, "x0 must be finite");
+    mppi_status_t s = sticky_check(c);
+    if (s) return s;
+    const float* eps = noise;
+    if (!noise) {
+        MPPI_CUDA(launch_noise(c, seed, step, c.d_eps, true), "noise_kernel launch");
+        eps = c.d_eps;
+    } else {
+        MPPI_CUDA(cudaMemcpyAsync(&c.d_stats->min_key, c.d_key_init, sizeof(long long),
+                                  cudaMemcpyDeviceToDevice, c.stream), "min-key reset");
+    }
+    MPPI_CUDA(launch_rollout(c, x0, U, eps, costs_out), "rollout_kernel launch");
+    *eps_used = eps;
+    return MPPI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t mppi_abi_version(void) { return MPPI_ABI_VERSION; }
+
+const char* mppi_last_error(void) { return g_err.c_str(); }
+
+const char* mppi_status_string(mppi_status_t s) {
+    switch (s) {
+        case MPPI_OK: return "MPPI_OK";
+        case MPPI_ERR_INVALID_ARG: return "MPPI_ERR_INVALID_ARG";
+        case MPPI_ERR_NOT_SPD: return "MPPI_ERR_NOT_SPD";
+        case MPPI_ERR_OOM: return "MPPI_ERR_OOM";
+        case MPPI_ERR_CUDA: return "MPPI_ERR_CUDA";
+        case MPPI_ERR_UNSUPPORTED: return "MPPI_ERR_UNSUPPORTED";
+        default: return "MPPI_ERR_UNKNOWN";
+    }
+}
+
+mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* cost, int64_t K,
+                          int32_t T, float dt, float lambda, float nu, int32_t m,
+                          const double* Sigma, const double* R, const mppi_dist_t* dist,
+                          void* cuda_stream, mppi_ctx** out) {
+    g_err.clear();
+    if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!dynamics || !cost || !Sigma || !R)
+        return fail(MPPI_ERR_INVALID_ARG, "dynamics, cost, Sigma and R must be non-NULL");
+    if (dynamics->struct_size != sizeof(mppi_dynamics_t) || cost->struct_size != sizeof(mppi_cost_t))
+        return fail(MPPI_ERR_INVALID_ARG, "struct_size mismatch (dynamics %u vs %zu, cost %u vs %zu)",
+                    dynamics->struct_size, sizeof(mppi_dynamics_t), cost->struct_size, sizeof(mppi_cost_t));
+    const int plant = (int)dynamics->plant;
+    if (plant < MPPI_PLANT_CARTPOLE || plant > MPPI_PLANT_LINEAR)
+        return fail(MPPI_ERR_INVALID_ARG, "unknown plant %d", plant);
+    if (plant == MPPI_PLANT_LINEAR) {
+        if (m != 1 && m != 2 && m != 4) return fail(MPPI_ERR_INVALID_ARG, "linear plant: m must be 1, 2 or 4");
+    } else if (m != plant_control_dim(plant)) {
+        return fail(MPPI_ERR_INVALID_ARG, "m = %d but the plant has %d controls", m, plant_control_dim(plant));
+    }
+    if (K < 1 || K > INT_MAX) return fail(MPPI_ERR_INVALID_ARG, "K must be in [1, 2^31)");
+    if (T < 1 || T > 4096) return fail(MPPI_ERR_INVALID_ARG, "T must be in [1, 4096]");
+    if (!is_fin(dt) || !(dt > 0)) return fail(MPPI_ERR_INVALID_ARG, "dt must be finite and > 0");
+    if (!is_fin(lambda) || !(lambda > 0)) return fail(MPPI_ERR_INVALID_ARG, "lambda must be finite and > 0");
+    if (!is_fin(nu) || !(nu >= 1)) return fail(MPPI_ERR_INVALID_ARG, "nu must be finite and >= 1");
+    if (!is_fin(cost->penalty)) return fail(MPPI_ERR_INVALID_ARG, "penalty must be finite");
+    int rank = 0, world = 1;
+    if (dist) {
+        rank = dist->rank;
+        world = dist->world;
+        if (world < 1 || rank < 0 || rank >= world)
+            return fail(MPPI_ERR_INVALID_ARG, "dist: need 0 <= rank < world");
+    }
+    if (K % world) return fail(MPPI_ERR_INVALID_ARG, "K = %lld not divisible by world = %d", (long long)K, world);
+    const int64_t K_loc = K / world;
+    if (K_loc % 4) return fail(MPPI_ERR_INVALID_ARG, "K/world = %lld must be a multiple of 4", (long long)K_loc);
+    double L[16], LR[16];
+    if (!cholesky64(Sigma, m, L)) return fail(MPPI_ERR_NOT_SPD, "Sigma is not symmetric positive definite");
+    if (!cholesky64(R, m, LR)) return fail(MPPI_ERR_NOT_SPD, "R is not symmetric positive definite");
+
+    mppi_ctx* ctx = new (std::nothrow) mppi_ctx();
+    if (!ctx) return fail(MPPI_ERR_OOM, "host allocation failed");
+    Ctx& c = ctx->c;
+    c.plant = plant;
+    c.n = plant_state_dim(plant);
+    c.m = m;
+    c.T = T;
+    c.K = K;
+    c.K_loc = K_loc;
+    c.rank = rank;
+    c.world = world;
+    c.k_offset = (int64_t)rank * K_loc;
+    c.dt = dt;
+    c.lambda = lambda;
+    c.nu = nu;
+    c.c1 = (float)(0.5 * (1.0 - 1.0 / (double)nu));   // (1 - 1/nu)/2
+    c.penalty = cost->penalty;
+    c.stream = (cudaStream_t)cuda_stream;
+    const double s = sqrt((double)nu);
+    bool diag = true;
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) {
+            c.sL[i * m + j] = (float)(s * L[i * m + j]);
+            c.R[i * m + j] = (float)R[i * m + j];
+            if (i != j && (L[i * m + j] != 0.0 || R[i * m + j] != 0.0)) diag = false;
+        }
+    c.diag = diag;
+    mppi_status_t st = digest_params(c, dynamics, cost);
+    if (st) { delete ctx; return st; }
+
+    cudaError_t e = cudaGetDevice(&c.device);
+    if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaGetDevice (no CUDA device?)"); }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    // weighted-noise reduction grid: ~8 resident 256-thread CTAs per SM over (chunks x t-tiles)
+    const int64_t ncols = K_loc * m / 4;
+    const int ttiles = (T + kWsumTT - 1) / kWsumTT;
+    int64_t target = (int64_t)sms * 8;
+    int64_t nch = (target + ttiles - 1) / ttiles;
+    const int64_t max_ch = (ncols + kWsumThreads - 1) / kWsumThreads;
+    if (nch > max_ch) nch = max_ch;
+    if (nch < 1) nch = 1;
+    c.cols_per_chunk = (ncols + nch - 1) / nch;
+    c.n_chunks = (int)((ncols + c.cols_per_chunk - 1) / c.cols_per_chunk);
+
+    mppi_status_t a;
+    if ((a = dalloc(c, &c.d_eps, (size_t)T * K_loc * m, "noise")) ||
+        (a = dalloc(c, &c.d_costs, (size_t)K_loc, "costs")) ||
+        (a = dalloc(c, &c.d_key_init, 1, "key init")) ||
+        (a = dalloc(c, &c.d_part, (size_t)c.n_chunks * T * m, "partials")) ||
+        (a = dalloc(c, &c.d_eta_part, (size_t)c.n_chunks, "eta partials")) ||
+        (a = dalloc(c, &c.d_stats, 1, "stats")) ||
+        (a = dalloc(c, &c.d_U, (size_t)T * m, "U staging")) ||
+        (a = dalloc(c, &c.d_obs, (size_t)(c.n_obs_pairs > 0 ? c.n_obs_pairs : 1), "obstacles"))) {
+        free_ctx(c);
+        delete ctx;
+        return a;
+    }
+    e = cudaMallocHost((void**)&c.h_U_pinned, (size_t)T * m * sizeof(float));
+    if (e != cudaSuccess) { free_ctx(c); delete ctx; return fail(MPPI_ERR_OOM, "pinned staging"); }
+    const long long kinit = LLONG_MAX;
+    DeviceStats st0;
+    st0.min_key = LLONG_MAX;
+    st0.eta = 0.0f;
+    st0.pad = 0.0f;
+    if ((e = cudaMemcpy(c.d_key_init, &kinit, sizeof(kinit), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(c.d_stats, &st0, sizeof(st0), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (c.n_obs_pairs > 0 &&
+         (e = cudaMemcpy(c.d_obs, c.obs_host.data(), c.n_obs_pairs * sizeof(float4), cudaMemcpyHostToDevice)) != cudaSuccess)) {
+        free_ctx(c);
+        delete ctx;
+        return cuda_fail(e, "workspace init");
+    }
+    *out = ctx;
+    return MPPI_OK;
+}
+
+void mppi_destroy(mppi_ctx* ctx) {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->c.stream);
+    free_ctx(ctx->c);
+    delete ctx;
+}
+
+mppi_status_t mppi_info(const mppi_ctx* ctx, mppi_info_t* out) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
+    const Ctx& c = ctx->c;
+    out->n = c.n;
+    out->m = c.m;
+    out->T = c.T;
+    out->plant = c.plant;
+    out->K = c.K;
+    out->K_loc = c.K_loc;
+    out->k_offset = c.k_offset;
+    out->n_chunks = c.n_chunks;
+    out->reserved = 0;
+    out->workspace_bytes = c.workspace_bytes;
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_set_stream(mppi_ctx* ctx, void* cuda_stream) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    ctx->c.stream = (cudaStream_t)cuda_stream;
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed, uint64_t step,
+                            const float* noise) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (c.world != 1) return fail(MPPI_ERR_UNSUPPORTED, "mppi_optimize needs world == 1; use the split-phase calls");
+    c.last_launches = 0;
+    const float* eps = nullptr;
+    if (mppi_status_t s = do_rollout(c, x0, U, seed, step, noise, nullptr, &eps)) return s;
+    MPPI_CUDA(launch_wsum(c, eps, &c.d_stats->min_key), "wsum_kernel launch");
+    MPPI_CUDA(launch_finalize(c, nullptr, nullptr, U), "finalize_kernel launch");
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_optimize_host(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed, uint64_t step) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (!U) return fail(MPPI_ERR_INVALID_ARG, "U is NULL");
+    const size_t bytes = (size_t)c.T * c.m * sizeof(float);
+    memcpy(c.h_U_pinned, U, bytes);
+    MPPI_CUDA(cudaMemcpyAsync(c.d_U, c.h_U_pinned, bytes, cudaMemcpyHostToDevice, c.stream), "U H2D");
+    if (mppi_status_t s = mppi_optimize(ctx, x0, c.d_U, seed, step, nullptr)) return s;
+    MPPI_CUDA(cudaMemcpyAsync(c.h_U_pinned, c.d_U, bytes, cudaMemcpyDeviceToHost, c.stream), "U D2H");
+    MPPI_CUDA(cudaStreamSynchronize(c.stream), "stream sync");
+    memcpy(U, c.h_U_pinned, bytes);
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_rollout_costs(mppi_ctx* ctx, const float* x0, const float* U, uint64_t seed,
+                                 uint64_t step, const float* noise, float* costs, int64_t* min_key) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    c.last_launches = 0;
+    const float* eps = nullptr;
+    if (mppi_status_t s = do_rollout(c, x0, U, seed, step, noise, costs, &eps)) return s;
+    c.last_eps = eps;  // mppi_accumulate reads the same noise again
+    if (min_key)
+        MPPI_CUDA(cudaMemcpyAsync(min_key, &c.d_stats->min_key, sizeof(long long),
+                                  cudaMemcpyDeviceToDevice, c.stream), "min key copy");
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, float* buf) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (!buf) return fail(MPPI_ERR_INVALID_ARG, "buf is NULL");
+    if (mppi_status_t s = sticky_check(c)) return s;
+    c.last_launches = 0;
+    const long long* key = global_min_key ? (const long long*)global_min_key : &c.d_stats->min_key;
+    MPPI_CUDA(launch_wsum(c, c.last_eps ? c.last_eps : c.d_eps, key), "wsum_kernel launch");
+    MPPI_CUDA(launch_finalize(c, nullptr, buf, nullptr), "finalize_kernel launch");
+    if (global_min_key)
+        MPPI_CUDA(cudaMemcpyAsync(&c.d_stats->min_key, key, sizeof(long long),
+                                  cudaMemcpyDeviceToDevice, c.stream), "global key copy");
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_apply(mppi_ctx* ctx, float* U, const float* buf) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (!U || !buf) return fail(MPPI_ERR_INVALID_ARG, "U and buf must be non-NULL");
+    if (mppi_status_t s = sticky_check(c)) return s;
+    c.last_launches = 0;
+    MPPI_CUDA(launch_finalize(c, buf, nullptr, U), "finalize_kernel launch");
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_shift(mppi_ctx* ctx, float* U, const float* u_init) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (!U || !u_init) return fail(MPPI_ERR_INVALID_ARG, "U and u_init must be non-NULL");
+    if (!all_finite(u_init, c.m)) return fail(MPPI_ERR_INVALID_ARG, "u_init must be finite");
+    if (mppi_status_t s = sticky_check(c)) return s;
+    c.last_launches = 0;
+    MPPI_CUDA(launch_shift(c, U, u_init), "shift_kernel launch");
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_noise(mppi_ctx* ctx, uint64_t seed, uint64_t step, float* out) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
+    if (mppi_status_t s = sticky_check(c)) return s;
+    c.last_launches = 0;
+    MPPI_CUDA(launch_noise(c, seed, step, out, false), "noise_kernel launch");
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_plant_step(mppi_ctx* ctx, float* x, const float* u, int32_t* crashed, float* q_out) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (!x || !u) return fail(MPPI_ERR_INVALID_ARG, "x and u must be non-NULL");
+    const float q = host_plant_step(c, x, u, crashed);
+    if (q_out) *q_out = q;
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_get_stats(mppi_ctx* ctx, mppi_stats_t* out) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
+    Ctx& c = ctx->c;
+    MPPI_CUDA(cudaStreamSynchronize(c.stream), "stream sync");
+    DeviceStats h;
+    MPPI_CUDA(cudaMemcpy(&h, c.d_stats, sizeof(h), cudaMemcpyDeviceToHost), "stats D2H");
+    int b = (int)(h.min_key >> 32);
+    b = b >= 0 ? b : (b ^ 0x7fffffff);
+    float smin;
+    memcpy(&smin, &b, sizeof(smin));
+    out->k_star = (int64_t)(uint32_t)(h.min_key & 0xffffffffLL);
+    out->s_min = smin;
+    out->eta = h.eta;
+    return MPPI_OK;
+}
+
+int32_t mppi_last_launch_count(const mppi_ctx* ctx) { return ctx ? ctx->c.last_launches : 0; }
+
+static mppi_status_t drain_profile(Ctx& c) {
+    for (auto& p : c.ev_pending) {
+        float ms = 0.0f;
+        cudaError_t e = cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventElapsedTime");
+        c.prof_ms[p.first] += ms;
+        c.prof_n[p.first] += 1;
+        c.ev_pool.push_back(p.second.first);
+        c.ev_pool.push_back(p.second.second);
+    }
+    c.ev_pending.clear();
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_profile_enable(mppi_ctx* ctx, int32_t enable) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    MPPI_CUDA(cudaStreamSynchronize(c.stream), "stream sync");
+    if (mppi_status_t s = drain_profile(c)) return s;
+    for (int i = 0; i < MPPI_KERNEL_KINDS; ++i) { c.prof_ms[i] = 0.0; c.prof_n[i] = 0; }
+    c.prof = enable != 0;
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_profile_read(mppi_ctx* ctx, mppi_kernel_times_t* out) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
+    Ctx& c = ctx->c;
+    MPPI_CUDA(cudaStreamSynchronize(c.stream), "stream sync");
+    if (mppi_status_t s = drain_profile(c)) return s;
+    for (int i = 0; i < MPPI_KERNEL_KINDS; ++i) {
+        out->total_ms[i] = c.prof_ms[i];
+        out->launches[i] = c.prof_n[i];
+        c.prof_ms[i] = 0.0;
+        c.prof_n[i] = 0;
+    }
+    return MPPI_OK;
+}
+
+}  // extern "C"

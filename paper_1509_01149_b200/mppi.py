@@ -1,0 +1,195 @@
+"""Python face of libmppi_b200.so: one MPPI optimisation step on a B200.
+
+Thin binding over include/mppi.h with the same names (mppi_create -> MPPI(...),
+mppi_optimize -> MPPI.optimize, ...).  PyTorch provides device memory and the stream;
+every step of the path runs in the library's CUDA kernels.  There is no CPU fallback.
+"""
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _capi as A
+from .plants import PlantSpec
+
+
+def _fptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _check_dev(t, shape, dtype, name):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("%s must be a CUDA tensor" % name)
+    if t.dtype != dtype or not t.is_contiguous() or tuple(t.shape) != tuple(shape):
+        raise ValueError("%s must be a contiguous %s tensor of shape %s (got %s %s)"
+                         % (name, dtype, tuple(shape), t.dtype, tuple(t.shape)))
+
+
+def _host_f32(a, n, name):
+    a = np.ascontiguousarray(np.asarray(a, np.float32).reshape(-1))
+    if a.size != n:
+        raise ValueError("%s must have %d entries" % (name, n))
+    return a
+
+
+class MPPI:
+    """mppi_create(dynamics, cost, K, T, dt, lambda, nu, Sigma, R) — PAPER.md:346-352."""
+
+    def __init__(self, plant, K, T, dt, lam, nu, Sigma, R, dynamics=None, cost=None,
+                 obstacles=None, penalty=1e30, linear=None, rank=0, world=1, device=None):
+        self.lib = A.lib()
+        if device is not None:
+            torch.cuda.set_device(device)
+        self.spec = PlantSpec(plant, dynamics, cost, obstacles, penalty, linear)
+        self.n, self.m = self.spec.n, self.spec.m
+        self.K, self.T = int(K), int(T)
+        self.Sigma = np.ascontiguousarray(np.asarray(Sigma, np.float64).reshape(self.m, self.m))
+        self.R = np.ascontiguousarray(np.asarray(R, np.float64).reshape(self.m, self.m))
+        self._stream = torch.cuda.current_stream().cuda_stream
+        d = A.dist_t(rank, world)
+        ctx = C.c_void_p()
+        A.check(self.lib.mppi_create(
+            C.byref(self.spec.dyn), C.byref(self.spec.cost), self.K, self.T, dt, lam, nu, self.m,
+            self.Sigma.ctypes.data_as(C.POINTER(C.c_double)),
+            self.R.ctypes.data_as(C.POINTER(C.c_double)), C.byref(d),
+            C.c_void_p(self._stream), C.byref(ctx)))
+        self.ctx = ctx
+        inf = self.info()
+        self.K_loc, self.k_offset = inf.K_loc, inf.k_offset
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    # ------------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.mppi_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self):
+        out = A.info_t()
+        A.check(self.lib.mppi_info(self.ctx, C.byref(out)))
+        return out
+
+    def _sync_stream(self):
+        s = torch.cuda.current_stream().cuda_stream
+        if s != self._stream:
+            A.check(self.lib.mppi_set_stream(self.ctx, C.c_void_p(s)))
+            self._stream = s
+
+    def _x0(self, x0):
+        return _host_f32(x0.detach().cpu().numpy() if isinstance(x0, torch.Tensor) else x0,
+                         self.n, "x0")
+
+    # ------------------------------------------------------------------ the step
+    def optimize(self, x0, U, seed=0, step=0, noise=None):
+        """mppi_optimize: U (CUDA float32 [T][m]) updated in place."""
+        _check_dev(U, (self.T, self.m), torch.float32, "U")
+        if noise is not None:
+            _check_dev(noise, (self.T, self.K_loc, self.m), torch.float32, "noise")
+        self._sync_stream()
+        x = self._x0(x0)
+        A.check(self.lib.mppi_optimize(self.ctx, x.ctypes.data_as(C.POINTER(C.c_float)), _fptr(U),
+                                       seed, step, _fptr(noise) if noise is not None else None))
+        return U
+
+    def optimize_host(self, x0, U, seed=0, step=0):
+        """mppi_optimize_host: U is a host float32 array [T][m], updated in place (synchronous)."""
+        if not (isinstance(U, np.ndarray) and U.dtype == np.float32 and U.flags.c_contiguous
+                and U.shape == (self.T, self.m)):
+            raise ValueError("U must be a C-contiguous float32 numpy array of shape (T, m)")
+        self._sync_stream()
+        x = self._x0(x0)
+        A.check(self.lib.mppi_optimize_host(self.ctx, x.ctypes.data_as(C.POINTER(C.c_float)),
+                                            U.ctypes.data_as(C.POINTER(C.c_float)), seed, step))
+        return U
+
+    def rollout_costs(self, x0, U, seed=0, step=0, noise=None, costs=None, min_key=None):
+        _check_dev(U, (self.T, self.m), torch.float32, "U")
+        if noise is not None:
+            _check_dev(noise, (self.T, self.K_loc, self.m), torch.float32, "noise")
+        if costs is None:
+            costs = torch.empty(self.K_loc, dtype=torch.float32, device=U.device)
+        _check_dev(costs, (self.K_loc,), torch.float32, "costs")
+        if min_key is None:
+            min_key = torch.empty(1, dtype=torch.int64, device=U.device)
+        _check_dev(min_key, (1,), torch.int64, "min_key")
+        self._sync_stream()
+        x = self._x0(x0)
+        A.check(self.lib.mppi_rollout_costs(
+            self.ctx, x.ctypes.data_as(C.POINTER(C.c_float)), _fptr(U), seed, step,
+            _fptr(noise) if noise is not None else None, _fptr(costs), _fptr(min_key)))
+        return costs, min_key
+
+    def accumulate(self, global_min_key=None, buf=None):
+        if buf is None:
+            buf = torch.empty(1 + self.T * self.m, dtype=torch.float32, device=self.device)
+        _check_dev(buf, (1 + self.T * self.m,), torch.float32, "buf")
+        if global_min_key is not None:
+            _check_dev(global_min_key, (1,), torch.int64, "global_min_key")
+        self._sync_stream()
+        A.check(self.lib.mppi_accumulate(
+            self.ctx, _fptr(global_min_key) if global_min_key is not None else None, _fptr(buf)))
+        return buf
+
+    def apply(self, U, buf):
+        _check_dev(U, (self.T, self.m), torch.float32, "U")
+        _check_dev(buf, (1 + self.T * self.m,), torch.float32, "buf")
+        self._sync_stream()
+        A.check(self.lib.mppi_apply(self.ctx, _fptr(U), _fptr(buf)))
+        return U
+
+    # ------------------------------------------------------------------ helpers
+    def shift(self, U, u_init=None):
+        _check_dev(U, (self.T, self.m), torch.float32, "U")
+        ui = _host_f32(np.zeros(self.m) if u_init is None else u_init, self.m, "u_init")
+        self._sync_stream()
+        A.check(self.lib.mppi_shift(self.ctx, _fptr(U), ui.ctypes.data_as(C.POINTER(C.c_float))))
+        return U
+
+    def noise(self, seed=0, step=0, out=None):
+        if out is None:
+            out = torch.empty((self.T, self.K_loc, self.m), dtype=torch.float32, device=self.device)
+        _check_dev(out, (self.T, self.K_loc, self.m), torch.float32, "out")
+        self._sync_stream()
+        A.check(self.lib.mppi_noise(self.ctx, seed, step, _fptr(out)))
+        return out
+
+    def plant_step(self, x, u, crashed=0):
+        """mppi_plant_step: host fp32 Euler step; returns (x', q(x'), crashed')."""
+        xs = _host_f32(x, self.n, "x").copy()
+        us = _host_f32(u, self.m, "u")
+        c = C.c_int32(int(crashed))
+        q = C.c_float()
+        A.check(self.lib.mppi_plant_step(self.ctx, xs.ctypes.data_as(C.POINTER(C.c_float)),
+                                         us.ctypes.data_as(C.POINTER(C.c_float)), C.byref(c),
+                                         C.byref(q)))
+        return xs, q.value, c.value
+
+    def stats(self):
+        out = A.stats_t()
+        A.check(self.lib.mppi_get_stats(self.ctx, C.byref(out)))
+        return dict(k_star=out.k_star, s_min=out.s_min, eta=out.eta)
+
+    def profile_enable(self, enable=True):
+        A.check(self.lib.mppi_profile_enable(self.ctx, 1 if enable else 0))
+
+    def profile_read(self):
+        """{kernel: (total_ms, launches)} since the last read (synchronous)."""
+        out = A.kernel_times_t()
+        A.check(self.lib.mppi_profile_read(self.ctx, C.byref(out)))
+        return {n: (out.total_ms[i], out.launches[i]) for i, n in enumerate(A.KERNEL_NAMES)}
+
+    def last_launch_count(self):
+        return self.lib.mppi_last_launch_count(self.ctx)
+
+
+def from_workload(w, K=None, world=1, rank=0, **kw):
+    """MPPI context for an mppi_inputs.Workload (configs C1-C5)."""
+    obstacles = w.obstacles if w.plant == "quadrotor" else None
+    return MPPI(w.plant, K or w.K, w.T, w.dt, w.lam, w.nu, w.Sigma, w.R, obstacles=obstacles,
+                rank=rank, world=world, **kw)

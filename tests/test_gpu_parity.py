@@ -1,0 +1,359 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+inputs.  Bars (BASELINE.json north_star):
+  * noise eps and sample indices: bit-exact
+  * per-sample costs: |dS| <= 1e-4 max(|S|, 1) on samples the oracle marks well-conditioned
+    (both fp32 twins within 1e-5 of fp64, A19); the excluded fraction is reported/bounded
+  * U: within 1e-5 absolute (decoupled check A20(i) always; coupled check A20(ii) when the
+    first-order error bound evaluated with the actual cost differences allows it)
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from mppi_inputs import get  # noqa: E402
+from paper_1509_01149_b200 import MPPI, from_workload  # noqa: E402
+
+COST_RTOL = 1e-4
+U_ATOL = 1e-5
+
+
+def oracle_problem(oracle, w, lam=None, nu=None, T=None):
+    return oracle.Problem(w.plant, T=T or w.T, dt=w.dt, lam=lam or w.lam, nu=nu or w.nu,
+                          Sigma=w.Sigma, R=w.R,
+                          obstacles=w.obstacles if w.plant == "quadrotor" else None)
+
+
+def cuda_u(w):
+    return torch.tensor(w.U0, device="cuda")
+
+
+# ----------------------------------------------------------------------------- noise
+@pytest.mark.parametrize("cfg,K,T", [("C1", 256, 50), ("C3", 1024, 20), ("C4", 2048, 12)])
+@pytest.mark.parametrize("seed,step", [(1, 0), (0xDEADBEEFCAFEF00D, 7), (3, 0x100000002)])
+def test_noise_bit_exact(oracle, cfg, K, T, seed, step):
+    w = get(cfg)
+    m = MPPI(w.plant, K, T, w.dt, w.lam, w.nu, w.Sigma, w.R, obstacles=w.obstacles if w.plant == "quadrotor" else None)
+    eps = m.noise(seed, step).cpu().numpy()
+    ref = oracle.noise(seed, step, T, K, w.m)
+    assert eps.view(np.uint32).tobytes() == ref.view(np.uint32).tobytes()
+
+
+def test_noise_shards_are_slices_of_the_global_stream(oracle):
+    w = get("C4")
+    K, T = 4096, 6
+    full = oracle.noise(5, 2, T, K, 4)
+    for rank in range(4):
+        m = MPPI("quadrotor", K, T, w.dt, w.lam, w.nu, w.Sigma, w.R, obstacles=w.obstacles,
+                 rank=rank, world=4)
+        sh = m.noise(5, 2).cpu().numpy()
+        assert np.array_equal(sh.view(np.uint32), full[:, rank * 1024:(rank + 1) * 1024].view(np.uint32))
+
+
+# ----------------------------------------------------------------------------- costs
+def _costs_parity(oracle, w, K, T=None, max_excluded=None, seed=None):
+    T = T or w.T
+    seed = w.seed if seed is None else seed
+    m = from_workload(w, K=K) if T == w.T else MPPI(
+        w.plant, K, T, w.dt, w.lam, w.nu, w.Sigma, w.R,
+        obstacles=w.obstacles if w.plant == "quadrotor" else None)
+    U0 = np.ascontiguousarray(w.U0[:T])
+    U = torch.tensor(U0, device="cuda")
+    costs, key = m.rollout_costs(w.x0, U, seed, 0)
+    costs = costs.cpu().numpy().astype(np.float64)
+    eps = oracle.noise(seed, 0, T, K, w.m)
+    pb = oracle_problem(oracle, w, T=T)
+    ok, ref = oracle.well_conditioned(pb, w.x0.astype(np.float64), U0, eps)
+    err = np.abs(costs - ref) / np.maximum(np.abs(ref), 1.0)
+    excluded = 1.0 - ok.mean()
+    bad = np.nonzero(ok & (err > COST_RTOL))[0]
+    assert bad.size == 0, "well-conditioned samples over 1e-4: %s (max err %.3g)" % (bad[:10], err[ok].max())
+    if max_excluded is not None:
+        assert excluded <= max_excluded, "excluded fraction %.4f" % excluded
+    return costs, ref, key, m, excluded, err
+
+
+def test_costs_c1_cartpole(oracle):
+    w = get("C1")
+    costs, ref, key, m, excl, err = _costs_parity(oracle, w, w.K, max_excluded=0.001)
+    # every sample of C1 (from rest) must be within tolerance, conditioning filter or not
+    assert err.max() <= COST_RTOL
+
+
+def test_costs_c2_cartpole_nu1000(oracle):
+    w = get("C2")
+    _costs_parity(oracle, w, 4096, max_excluded=0.05)
+
+
+def test_costs_c3_racecar(oracle):
+    w = get("C3")
+    _costs_parity(oracle, w, 4096, max_excluded=0.05)
+
+
+def test_costs_c4_quadrotor(oracle):
+    w = get("C4")
+    _costs_parity(oracle, w, 4096, max_excluded=0.05)
+
+
+def test_argmin_and_min_key(oracle):
+    w = get("C4")
+    costs, ref, key, m, _, _ = _costs_parity(oracle, w, 4096)
+    key = int(key.cpu().item())
+    k_gpu = key & 0xFFFFFFFF
+    assert k_gpu == int(np.argmin(costs)) and costs[k_gpu] == costs.min()
+    order = np.sort(ref)
+    dS = np.max(np.abs(costs - ref))
+    if order[1] - order[0] > 2 * dS:           # A21(ii): k* must match the oracle's
+        assert k_gpu == int(np.argmin(ref))
+
+
+# ----------------------------------------------------------------------------- U
+def _u_parity(oracle, w, K, lam=None, seed=1, coupled=True):
+    lam = lam or w.lam
+    m = MPPI(w.plant, K, w.T, w.dt, lam, w.nu, w.Sigma, w.R,
+             obstacles=w.obstacles if w.plant == "quadrotor" else None)
+    U = cuda_u(w)
+    costs, key = m.rollout_costs(w.x0, U, seed, 0)
+    eps_gpu = m.noise(seed, 0).cpu().numpy()
+    buf = m.accumulate()
+    m.apply(U, buf)
+    U_gpu = U.cpu().numpy().astype(np.float64)
+    # one-shot path gives the same bits as the split phase
+    U2 = cuda_u(w)
+    m.optimize(w.x0, U2, seed, 0)
+    assert torch.equal(U2, U)
+    pb = oracle_problem(oracle, w, lam=lam)
+    # (i) decoupled: oracle reduction on the GPU's costs and noise
+    Ud, kstar, smin, eta, wts = oracle.update(pb, costs.cpu().numpy().astype(np.float64), eps_gpu, w.U0)
+    assert np.max(np.abs(U_gpu - Ud)) <= U_ATOL
+    st = m.stats()
+    assert st["k_star"] == kstar
+    # (ii) coupled: the full fp64 oracle step, asserted when the first-order bound permits
+    ref = oracle.optimize(pb, w.x0, w.U0, oracle.noise(seed, 0, w.T, K, w.m))
+    dS = costs.cpu().numpy().astype(np.float64) - ref["costs"]
+    wbar = ref["weights"] / ref["weights"].sum()
+    du = math.sqrt(w.nu) * np.einsum("ij,tkj->tki", np.linalg.cholesky(w.Sigma), eps_gpu.astype(np.float64))
+    dev = np.abs(du - np.einsum("k,tki->ti", wbar, du)[:, None, :]).max(axis=(0, 2))
+    bound = np.sum(wbar * np.abs(dS) * dev) / lam
+    if coupled and bound <= 5e-6:
+        assert np.max(np.abs(U_gpu - ref["U"])) <= U_ATOL
+    return U_gpu, ref, bound
+
+
+def test_update_c1(oracle):
+    _u_parity(oracle, get("C1"), 256)
+
+
+def test_update_c3_racecar(oracle):
+    _u_parity(oracle, get("C3"), 4096)
+
+
+def test_update_c4_quadrotor(oracle):
+    _u_parity(oracle, get("C4"), 4096)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C3", "C4"])
+def test_update_nondegenerate_lambda(oracle, cfg):
+    """rerun at lambda = std_k(S~_k) so many samples carry weight (A20 decoupled)."""
+    w = get(cfg)
+    K = 256 if cfg == "C1" else 4096
+    pb = oracle_problem(oracle, w)
+    ref_costs = oracle.rollout_costs(pb, w.x0, w.U0, oracle.noise(1, 0, w.T, K, w.m))
+    _u_parity(oracle, w, K, lam=float(np.std(ref_costs)))
+
+
+def test_lambda_to_zero_is_bitwise_argmin_sample(oracle):
+    """P5 on the GPU: w_{k*} = expf(0) = 1, the rest underflow to +0, eta = 1, so
+    U' = fl(U + fl(sL * eps_{k*})) exactly in K4's op order; and k* matches the oracle."""
+    w = get("C1")
+    m = MPPI(w.plant, 256, w.T, w.dt, 1e-12, w.nu, w.Sigma, w.R)
+    U = cuda_u(w)
+    costs, key = m.rollout_costs(w.x0, U, 1, 0)
+    eps = m.noise(1, 0).cpu().numpy()
+    buf = m.accumulate()
+    m.apply(U, buf)
+    st = m.stats()
+    k = st["k_star"]
+    assert st["eta"] == 1.0
+    sL = np.float32(math.sqrt(w.nu) * math.sqrt(w.Sigma[0, 0]))
+    want = (w.U0[:, 0] + (sL * eps[:, k, 0]).astype(np.float32)).astype(np.float32)
+    assert np.array_equal(U.cpu().numpy()[:, 0], want)
+    ref_costs = oracle.rollout_costs(oracle_problem(oracle, w), w.x0, w.U0, oracle.noise(1, 0, w.T, 256, 1))
+    assert k == int(np.argmin(ref_costs))
+
+
+def test_lambda_to_infinity_is_noise_mean(oracle):
+    """P6: lambda = 1e30 -> every w = 1.0f exactly, eta = K exactly, U' = U + mean du."""
+    w = get("C3")
+    K = 4096
+    m = MPPI(w.plant, K, w.T, w.dt, 1e30, w.nu, w.Sigma, w.R)
+    U = cuda_u(w)
+    m.optimize(w.x0, U, 1, 0)
+    assert m.stats()["eta"] == float(K)
+    eps = oracle.noise(1, 0, w.T, K, 2).astype(np.float64)
+    want = w.U0 + math.sqrt(w.nu) * eps.mean(axis=1) @ np.linalg.cholesky(w.Sigma).T
+    assert np.max(np.abs(U.cpu().numpy() - want)) <= U_ATOL
+
+
+# ----------------------------------------------------------------------------- modes and invariants
+def test_supplied_noise_equals_seeded_run():
+    """with `noise` supplied the seed is ignored and the result equals the seeded run."""
+    w = get("C4")
+    m = from_workload(w, K=2048)
+    U1 = cuda_u(w)
+    m.optimize(w.x0, U1, 9, 4)
+    eps = m.noise(9, 4)
+    U2 = cuda_u(w)
+    m.optimize(w.x0, U2, 12345, 0, noise=eps)
+    assert torch.equal(U1, U2)
+
+
+def test_determinism():
+    """P14: same (seed, step) -> bitwise-identical costs and U run to run (no float atomics)."""
+    w = get("C4")
+    m = from_workload(w, K=8192)
+    outs = []
+    for _ in range(3):
+        U = cuda_u(w)
+        c, k = m.rollout_costs(w.x0, U, 2, 3)
+        c = c.clone()
+        m.optimize(w.x0, U, 2, 3)
+        outs.append((c, U.clone(), int(k.item())))
+    for c, U, k in outs[1:]:
+        assert torch.equal(c, outs[0][0]) and torch.equal(U, outs[0][1]) and k == outs[0][2]
+
+
+def test_sharded_split_phase_matches_single_gpu():
+    """P13 emulated on one GPU (SURVEY §4 "fake backend"): G contexts with rank/world run their
+    shards; the host combines MIN of keys and SUM of [eta, A]; costs and noise are bitwise the
+    single-GPU ones and U agrees within 1e-6."""
+    w = get("C4")
+    K = 8192
+    single = from_workload(w, K=K)
+    U1 = cuda_u(w)
+    c1, k1 = single.rollout_costs(w.x0, U1, 4, 1)
+    c1 = c1.clone()
+    single.optimize(w.x0, U1, 4, 1)
+    for G in (2, 4):
+        ms = [from_workload(w, K=K, rank=r, world=G) for r in range(G)]
+        U = cuda_u(w)
+        outs = [m.rollout_costs(w.x0, U, 4, 1) for m in ms]
+        costs = torch.cat([o[0] for o in outs])
+        assert torch.equal(costs, c1)
+        key = torch.stack([o[1] for o in outs]).min(dim=0).values
+        assert int(key.item()) == int(k1.item())
+        bufs = [m.accumulate(key) for m in ms]
+        buf = torch.stack(bufs).sum(dim=0)
+        Us = []
+        for m in ms:
+            Ur = cuda_u(w)
+            m.apply(Ur, buf)
+            Us.append(Ur)
+        for Ur in Us[1:]:
+            assert torch.equal(Ur, Us[0])
+        assert torch.max(torch.abs(Us[0] - U1)).item() <= 1e-6
+
+
+def test_penalty_on_non_finite_noise():
+    """SURVEY A15 fault injection: NaN/Inf in supplied noise -> penalty cost, no error."""
+    w = get("C1")
+    m = from_workload(w)
+    eps = m.noise(1, 0)
+    eps[3, 7, 0] = float("nan")
+    eps[0, 9, 0] = float("inf")
+    costs, key = m.rollout_costs(w.x0, cuda_u(w), 0, 0, noise=eps)
+    c = costs.cpu().numpy()
+    assert c[7] == np.float32(1e30) and c[9] == np.float32(1e30)
+    assert np.all(np.isfinite(c))
+
+
+def test_shift_and_optimize_host(oracle):
+    w = get("C3")
+    m = from_workload(w, K=1024)
+    U = torch.tensor(np.random.default_rng(0).normal(size=(w.T, 2)).astype(np.float32), device="cuda")
+    ref = oracle.shift(U.cpu().numpy(), [0.1, 0.5])
+    m.shift(U, [0.1, 0.5])
+    assert np.array_equal(U.cpu().numpy(), ref.astype(np.float32))
+    Uh = np.ascontiguousarray(w.U0.copy())
+    m.optimize_host(w.x0, Uh, 3, 1)
+    Ud = cuda_u(w)
+    m.optimize(w.x0, Ud, 3, 1)
+    assert np.array_equal(Uh, Ud.cpu().numpy())
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C3", "C4"])
+def test_host_plant_step_matches_oracle(oracle, cfg):
+    w = get(cfg)
+    m = from_workload(w, K=256)
+    pb = oracle_problem(oracle, w)
+    x = w.x0.astype(np.float64)
+    xg = w.x0.copy()
+    rng = np.random.default_rng(1)
+    for t in range(50):
+        u = w.U0[0] + rng.normal(size=w.m) * 0.3
+        x, q, _ = oracle.plant_step(pb, x, u)
+        xg, qg, _ = m.plant_step(xg, u)
+        assert abs(qg - q) <= 1e-4 * max(abs(q), 1.0)
+    assert np.allclose(xg, x, rtol=1e-4, atol=1e-4)
+
+
+def test_linear_quadratic_closed_form_on_gpu(oracle):
+    """P10 end to end on the GPU: linear plant + quadratic cost -> the MC update converges to
+    the tilted-Gaussian mean (same construction as tests/test_oracle_step.py)."""
+    from lq_fixture import lq_setup
+    pb, x0, U, mu, Pinv = lq_setup(oracle)
+    lin = dict(A=[[0.0, 1.0], [-1.0, -0.3]], B=[[0.0], [1.0]], Q=[[2.0, 0.0], [0.0, 0.5]])
+    K = 1 << 16
+    m = MPPI("linear", K, pb.T, pb.dt, pb.lam, pb.nu, pb.Sigma, pb.R, linear=lin)
+    Ug = torch.tensor(U.astype(np.float32), device="cuda")
+    costs, _ = m.rollout_costs(x0, Ug, 11, 0)
+    ref = oracle.rollout_costs(pb, x0, U, oracle.noise(11, 0, pb.T, K, 1))
+    assert np.max(np.abs(costs.cpu().numpy() - ref) / np.maximum(np.abs(ref), 1)) <= COST_RTOL
+    m.optimize(x0, Ug, 11, 0)
+    ess_ref = oracle.optimize(pb, x0, U, oracle.noise(11, 0, pb.T, K, 1))
+    w_ = ess_ref["weights"] / ess_ref["weights"].sum()
+    ess = 1 / np.sum(w_ ** 2)
+    z = ((Ug.cpu().numpy() - U)[:, 0] - mu) / np.sqrt(np.diag(Pinv) / ess)
+    assert np.max(np.abs(z)) < 5.0
+
+
+# ----------------------------------------------------------------------------- full size (bench configuration)
+def test_full_size_c5_sampled(oracle):
+    """BASELINE config C5 at K = 2^22 in the bench's launch configuration: sampled noise rows
+    are bit-exact, sampled samples' costs match the oracle one by one, k* is the argmin of the
+    GPU costs, and the updated U is finite and equals the split-phase result."""
+    w = get("C5")
+    K = w.K
+    m = from_workload(w)
+    U = cuda_u(w)
+    costs, key = m.rollout_costs(w.x0, U, w.seed, 0)
+    eps = m.noise(w.seed, 0)                                 # [T][K][4] on device
+    rng = np.random.default_rng(0)
+    ks = np.sort(rng.choice(K, 64, replace=False))
+    ks = np.concatenate([ks, [0, K - 1]])
+    pb = oracle_problem(oracle, w)
+    for k in ks:
+        ref_eps = oracle.noise(w.seed, 0, w.T, 1, 4, k0=int(k))
+        got = eps[:, int(k):int(k) + 1, :].cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), ref_eps.view(np.uint32))
+        ok, ref = oracle.well_conditioned(pb, w.x0, w.U0, ref_eps)
+        g = float(costs[int(k)].item())
+        if ok[0]:
+            assert abs(g - ref[0]) <= COST_RTOL * max(abs(ref[0]), 1.0)
+    c = costs.cpu().numpy()
+    kk = int(key.item()) & 0xFFFFFFFF
+    assert c[kk] == c.min() and kk == int(np.argmin(c))
+    buf = m.accumulate()
+    Us = cuda_u(w)
+    m.apply(Us, buf)
+    U2 = cuda_u(w)
+    m.optimize(w.x0, U2, w.seed, 0)
+    assert torch.equal(Us, U2) and torch.isfinite(U2).all()
+    assert m.stats()["k_star"] == kk
