@@ -30,7 +30,8 @@ UNIT = "K*T/s"
 # FP32 FLOPs per sample-step of the rollout kernel (FADD + FMUL + 2 FFMA + 2 FADD2 + 2 FMUL2 +
 # 4 FFMA2 per thread, ncu sass counters / (K*T)); see DESIGN.md "Rollout FLOPs".  None -> not
 # yet measured for that plant (roofline falls back to the kernel's measured share only).
-ROLLOUT_FLOP_PER_SS = {"cartpole": None, "racecar": None, "quadrotor": None}
+ROLLOUT_FLOP_PER_SS = {"cartpole": None, "racecar": None,
+                       "quadrotor": 460.35}  # profiles/r1_ncu_full_c5_v0.txt (rollout v0)
 
 SM_COUNT_B200 = 148
 FP32_LANES_PER_SM = 128
