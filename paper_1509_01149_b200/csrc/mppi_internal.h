@@ -16,7 +16,9 @@ namespace mppi {
 
 constexpr int kRolloutThreads = 128;
 constexpr int kWsumThreads = 256;
-constexpr int kWsumTT = 8;  // timesteps per weighted-noise tile (register accumulators = 8 * m)
+constexpr int kWsumTT = 8;
+constexpr int kNoiseTT = 8;  // timesteps per noise thread
+constexpr int kEpsStages = 3;  // rollout: shared-memory ring depth for eps (cp.async 2 steps ahead)  // timesteps per weighted-noise tile (register accumulators = 8 * m)
 
 union PlantParamsU {
     CartpoleParams cartpole;
@@ -42,6 +44,7 @@ struct Ctx {
     bool diag = true;               // L and R both diagonal -> diagonal fast path
     float sL[16] = {0};             // sqrt(nu) * chol(Sigma), fp32, row-major m x m
     float R[16] = {0};              // control cost, fp32
+    float ad[4] = {0};              // diagonal path: (1 - 1/nu)/2 R_ii (sqrt(nu) L_ii)^2
     PlantParamsU params;            // pre-digested plant/cost parameters
     std::vector<float4> obs_host;   // negated obstacle pairs (host copy, for mppi_plant_step)
     int n_obs_pairs = 0;

@@ -43,6 +43,36 @@ __device__ __forceinline__ void store_eps(float* p, const float* z) {
     }
 }
 
+// Per-thread asynchronous copy of one noise element group (4m bytes) into shared memory
+// (LDGSTS; Ampere+ cp.async, non-blocking: no register is tied to the load).
+template <int M>
+__device__ __forceinline__ void cp_async_eps(float* smem_dst, const float* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    if constexpr (M == 4) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+    } else if constexpr (M == 2) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+    } else {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc) : "memory");
+    }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int M>
+__device__ __forceinline__ void load_smem_eps(const float* p, float* e) {
+    if constexpr (M == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(p);
+        e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
+    } else if constexpr (M == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(p);
+        e[0] = v.x; e[1] = v.y;
+    } else {
+        e[0] = *p;
+    }
+}
+
 // Order-preserving signed map of fp32 bits, then (cost, k) packed so that signed int64 MIN
 // picks the smallest cost and, among ties, the smallest global k.
 __device__ __forceinline__ long long cost_key(float s, unsigned k) {
@@ -73,21 +103,29 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // ------------------------------------------------------------------------------ K1 noise
-// One thread per (t, k): grid (ceil(K_loc/256), T).  Block (0,0) also resets the min key for the
-// rollout that follows on the same stream.
+// Grid (ceil(K_loc/256), ceil(T/kNoiseTT)): each thread owns one sample k and kNoiseTT timesteps
+// (independent Philox calls, unrolled by two for ILP), so the per-thread setup is amortised.
+// Block (0,0) also resets the min key for the rollout that follows on the same stream.
 template <int M>
-__global__ void __launch_bounds__(256) noise_kernel(float* __restrict__ eps, int K_loc,
+__global__ void __launch_bounds__(256) noise_kernel(float* __restrict__ eps, int K_loc, int T,
                                                     unsigned k_offset, unsigned step_lo,
                                                     unsigned step_hi, const PhiloxKeys keys,
                                                     long long* key_reset) {
     const int k = blockIdx.x * 256 + threadIdx.x;
-    const unsigned t = blockIdx.y;
-    if (key_reset && k == 0 && t == 0) *key_reset = LLONG_MAX;
+    const int t0 = blockIdx.y * kNoiseTT;
+    if (key_reset && k == 0 && t0 == 0) *key_reset = LLONG_MAX;
     if (k >= K_loc) return;
-    const uint4 w = philox4x32_10_dev(k_offset + (unsigned)k, t, step_lo, step_hi, keys);
-    float z[M];
-    bm32_normals<M>(w, z);
-    store_eps<M>(eps + ((size_t)t * K_loc + k) * M, z);
+    const unsigned kg = k_offset + (unsigned)k;
+    const int t1 = min(t0 + kNoiseTT, T);
+    const size_t row = (size_t)K_loc * M;
+    float* p = eps + ((size_t)t0 * K_loc + k) * M;
+#pragma unroll 2
+    for (int t = t0; t < t1; ++t, p += row) {
+        const uint4 w = philox4x32_10_dev(kg, (unsigned)t, step_lo, step_hi, keys);
+        float z[M];
+        bm32_normals<M>(w, z);
+        store_eps<M>(p, z);
+    }
 }
 
 // ------------------------------------------------------------------------------ K2 rollout
@@ -104,37 +142,51 @@ struct RolloutArgs {
     int K_loc;
     unsigned k_offset;
     float dt, c1, penalty;
-    float sL[16];           // sqrt(nu) chol(Sigma)
+    float sL[16];           // sqrt(nu) chol(Sigma), row-major M x M
     float R[16];
+    float sd[4];            // diagonal path: s_i = sL[i][i]
+    float ad[4];            // diagonal path: a_i = (1 - 1/nu)/2 R_ii s_i^2
     float x0[16];
     PP P;
 };
 
+// One sample per thread.  Per step t:
+//   v = U_t + du,  du = sqrt(nu) L eps[t][k]
+//   x <- x + F(x, v) dt,  S~ += q(x) + IS_t
+//   IS_t = (1 - 1/nu)/2 du'R du + U_t'R du + U_t'R U_t/2
+// With diagonal L and R (every shipped config) IS_t is evaluated as
+//   IS_t = K_t + sum_i e_i (a_i e_i + b_ti),  b_ti = s_i (R U_t)_i,  K_t = U_t'R U_t/2,
+// the same polynomial in eps with the per-t constants staged in shared memory.
+// eps[t][k] reaches the thread through a kEpsStages-deep shared-memory ring filled by per-thread
+// cp.async two steps ahead, so the HBM latency is hidden without tying up registers.
 template <class Plant, bool DIAG>
-__global__ void __launch_bounds__(kRolloutThreads)
+__global__ void __launch_bounds__(kRolloutThreads, 8)
     rollout_kernel(const RolloutArgs<typename Plant::Params> a) {
     constexpr int M = Plant::M;
     extern __shared__ float4 smem4[];
     float4* sObs = smem4;
-    float* sU = reinterpret_cast<float*>(smem4 + a.n_obs_pairs);  // U_t        [T][M]
-    float* sRU = sU + a.T * M;                                     // R U_t      [T][M]
-    float* sK = sRU + a.T * M;                                     // U_t'R U_t/2 [T]
+    float4* sU = smem4 + a.n_obs_pairs;   // U_t, zero padded to 4         [T]
+    float4* sB = sU + a.T;                // DIAG: s_i (R U_t)_i; else (R U_t)_i   [T]
+    float* sK = reinterpret_cast<float*>(sB + a.T);   // U_t'R U_t / 2   [T]
+    float* sRing = reinterpret_cast<float*>(smem4 + a.n_obs_pairs + 2 * a.T) +
+                   ((a.T + 3) & ~3);                  // eps ring [kEpsStages][blockDim][M]
     const int tid = threadIdx.x;
     for (int i = tid; i < a.n_obs_pairs; i += blockDim.x) sObs[i] = a.obs[i];
     for (int t = tid; t < a.T; t += blockDim.x) {
-        float u[M];
+        float u[4] = {0.0f, 0.0f, 0.0f, 0.0f}, bq[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
         for (int i = 0; i < M; ++i) u[i] = a.U[t * M + i];
         float kk = 0.0f;
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            float s = 0.0f;
+            float ru = 0.0f;
 #pragma unroll
-            for (int j = 0; j < M; ++j) s = fmaf(a.R[i * M + j], u[j], s);
-            sU[t * M + i] = u[i];
-            sRU[t * M + i] = s;
-            kk = fmaf(u[i], s, kk);
+            for (int j = 0; j < M; ++j) ru = fmaf(a.R[i * M + j], u[j], ru);
+            kk = fmaf(u[i], ru, kk);
+            bq[i] = DIAG ? a.sd[i] * ru : ru;
         }
+        sU[t] = make_float4(u[0], u[1], u[2], u[3]);
+        sB[t] = make_float4(bq[0], bq[1], bq[2], bq[3]);
         sK[t] = 0.5f * kk;
     }
     __syncthreads();
@@ -146,44 +198,64 @@ __global__ void __launch_bounds__(kRolloutThreads)
         st.load(a.x0, 0);
         const ObstacleView ob{sObs, a.n_obs_pairs};
         const size_t row = (size_t)a.K_loc * M;
-        const float* ep = a.eps + (size_t)k * M;
-        float e[M];
-        load_eps<M>(ep, e);
         float S = 0.0f;
-        for (int t = 0; t < a.T; ++t) {
-            float en[M];  // prefetch eps of step t+1 (clamped: the last prefetch re-reads row T-1)
-            load_eps<M>(ep + (size_t)min(t + 1, a.T - 1) * row, en);
-            float du[M], v[M];
+        auto one_step = [&](int t, const float* e) {
+            const float4 u4 = sU[t];
+            const float4 b4 = sB[t];
+            const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+            float v[M];
+            float is = sK[t];
+            if (DIAG) {
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                if (DIAG) {
-                    du[i] = a.sL[i * M + i] * e[i];
-                } else {
-                    float s = 0.0f;
-#pragma unroll
-                    for (int j = 0; j <= i; ++j) s = fmaf(a.sL[i * M + j], e[j], s);
-                    du[i] = s;
+                for (int i = 0; i < M; ++i) {
+                    v[i] = fmaf(a.sd[i], e[i], uu[i]);                 // U_t + s_i eps_i
+                    is = fmaf(e[i], fmaf(a.ad[i], e[i], bb[i]), is);   // IS_t
                 }
-                v[i] = sU[t * M + i] + du[i];               // u_i + du_{i,k}
-            }
-            const float q = st.step(v, a.dt, a.P, ob);      // x_{t+1}, q(x_{t+1})
-            float duRdu = 0.0f, uRdu = 0.0f;
+            } else {
+                float du[M];
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                if (DIAG) {
-                    duRdu = fmaf(a.R[i * M + i] * du[i], du[i], duRdu);
-                } else {
+                for (int i = 0; i < M; ++i) {
+                    float d = 0.0f;
+#pragma unroll
+                    for (int j = 0; j <= i; ++j) d = fmaf(a.sL[i * M + j], e[j], d);
+                    du[i] = d;
+                    v[i] = uu[i] + d;
+                }
+                float duRdu = 0.0f, uRdu = 0.0f;
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
 #pragma unroll
                     for (int j = 0; j < M; ++j) duRdu = fmaf(du[i] * a.R[i * M + j], du[j], duRdu);
+                    uRdu = fmaf(bb[i], du[i], uRdu);
                 }
-                uRdu = fmaf(sRU[t * M + i], du[i], uRdu);
+                is = fmaf(a.c1, duRdu, uRdu + is);
             }
-            // q~ = q + (1 - 1/nu)/2 du'R du + u'R du + u'R u / 2
-            S += q + fmaf(a.c1, duRdu, uRdu + sK[t]);
+            const float q = st.step(v, a.dt, a.P, ob);                 // x_{t+1}, q(x_{t+1})
+            S += q + is;                                               // S~ += q~
+        };
+        const float* ep = a.eps + (size_t)k * M;
+        float* ring = sRing + tid * M;                                 // slot stride: blockDim * M
+        const int slot_stride = blockDim.x * M;
 #pragma unroll
-            for (int i = 0; i < M; ++i) e[i] = en[i];
+        for (int j = 0; j < kEpsStages - 1; ++j) {                     // prologue: steps 0, 1
+            if (j < a.T) cp_async_eps<M>(ring + j * slot_stride, ep + (size_t)j * row);
+            cp_async_commit();
         }
-        if (!isfinite(S)) S = a.penalty;                     // SURVEY A15
+        int slot = 0;
+        for (int t = 0; t < a.T; ++t) {
+            const int ahead = t + kEpsStages - 1;
+            int fill = slot + kEpsStages - 1;
+            fill = fill >= kEpsStages ? fill - kEpsStages : fill;
+            if (ahead < a.T) cp_async_eps<M>(ring + fill * slot_stride, ep + (size_t)ahead * row);
+            cp_async_commit();
+            cp_async_wait<kEpsStages - 1>();                           // step t has landed
+            float e[M];
+            load_smem_eps<M>(ring + slot * slot_stride, e);
+            one_step(t, e);
+            slot = slot + 1 == kEpsStages ? 0 : slot + 1;
+        }
+        if (!isfinite(S)) S = a.penalty;                               // SURVEY A15
         a.costs[k] = S;
         if (a.costs_out) a.costs_out[k] = S;
         key = cost_key(S, a.k_offset + (unsigned)k);
@@ -396,14 +468,14 @@ static PhiloxKeys philox_key_schedule(uint64_t seed) {
 
 cudaError_t launch_noise(Ctx& c, uint64_t seed, uint64_t step, float* out, bool reset_key) {
     const PhiloxKeys keys = philox_key_schedule(seed);
-    const dim3 grid((unsigned)((c.K_loc + 255) / 256), (unsigned)c.T);
+    const dim3 grid((unsigned)((c.K_loc + 255) / 256), (unsigned)((c.T + kNoiseTT - 1) / kNoiseTT));
     ProfScope prof(c, MPPI_KERNEL_NOISE);
     long long* kr = reset_key ? reinterpret_cast<long long*>(&c.d_stats->min_key) : nullptr;
     const unsigned ko = (unsigned)c.k_offset, slo = (unsigned)step, shi = (unsigned)(step >> 32);
     switch (c.m) {
-        case 1: noise_kernel<1><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, ko, slo, shi, keys, kr); break;
-        case 2: noise_kernel<2><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, ko, slo, shi, keys, kr); break;
-        case 4: noise_kernel<4><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, ko, slo, shi, keys, kr); break;
+        case 1: noise_kernel<1><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, c.T, ko, slo, shi, keys, kr); break;
+        case 2: noise_kernel<2><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, c.T, ko, slo, shi, keys, kr); break;
+        case 4: noise_kernel<4><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, c.T, ko, slo, shi, keys, kr); break;
         default: return cudaErrorInvalidValue;
     }
     c.last_launches++;
@@ -428,10 +500,15 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     a.c1 = c.c1;
     a.penalty = c.penalty;
     for (int i = 0; i < 16; ++i) { a.sL[i] = c.sL[i]; a.R[i] = c.R[i]; a.x0[i] = 0.0f; }
+    for (int i = 0; i < 4; ++i) {
+        a.sd[i] = i < c.m ? c.sL[i * c.m + i] : 0.0f;
+        a.ad[i] = i < c.m ? c.ad[i] : 0.0f;
+    }
     for (int i = 0; i < c.n && i < 16; ++i) a.x0[i] = x0[i];
     a.P = P;
-    const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) +
-                        (size_t)(2 * c.T * Plant::M + c.T) * sizeof(float);
+    const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * 2 * sizeof(float4) +
+                        (size_t)((c.T + 3) & ~3) * sizeof(float) +
+                        (size_t)kEpsStages * kRolloutThreads * Plant::M * sizeof(float);
     auto kern = rollout_kernel<Plant, DIAG>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

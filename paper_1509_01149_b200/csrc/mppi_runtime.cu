@@ -330,6 +330,8 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
             if (i != j && (L[i * m + j] != 0.0 || R[i * m + j] != 0.0)) diag = false;
         }
     c.diag = diag;
+    for (int i = 0; i < m; ++i)   // IS_t = K_t + sum_i e_i (a_i e_i + b_ti) on the diagonal path
+        c.ad[i] = (float)(0.5 * (1.0 - 1.0 / (double)nu) * R[i * m + i] * (s * L[i * m + i]) * (s * L[i * m + i]));
     mppi_status_t st = digest_params(c, dynamics, cost);
     if (st) { delete ctx; return st; }
 
