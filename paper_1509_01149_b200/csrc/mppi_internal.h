@@ -18,7 +18,14 @@ constexpr int kRolloutThreads = 128;
 constexpr int kWsumThreads = 256;
 constexpr int kWsumTT = 8;
 constexpr int kNoiseTT = 8;  // timesteps per noise thread
-constexpr int kEpsStages = 3;  // rollout: shared-memory ring depth for eps (cp.async 2 steps ahead)  // timesteps per weighted-noise tile (register accumulators = 8 * m)
+constexpr int kMaxStaticPairs = 32;  // quadrotor: obstacle pairs compiled as a constant up to here
+
+// per-timestep constants of the rollout staged in shared memory (one 48-byte record per t)
+struct StepRec {
+    float4 u;  // U_t (zero padded to 4)
+    float4 b;  // diagonal path: s_i (R U_t)_i; general path: (R U_t)_i
+    float4 k;  // .x = U_t'R U_t / 2
+};  // timesteps per weighted-noise tile (register accumulators = 8 * m)
 
 union PlantParamsU {
     CartpoleParams cartpole;
@@ -87,6 +94,7 @@ cudaError_t launch_rollout(Ctx& c, const float* x0, const float* U, const float*
 cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key);
 cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* U);
 cudaError_t launch_shift(Ctx& c, float* U, const float* u_init);
+int wsum_blocks_per_sm(int m);  // resident wsum CTAs per SM (occupancy API)
 
 // host plant step (mppi_runtime.cu uses it for mppi_plant_step)
 float host_plant_step(const Ctx& c, float* x, const float* u, int32_t* crashed);

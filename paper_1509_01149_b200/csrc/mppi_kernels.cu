@@ -13,6 +13,7 @@
 // reproducible run to run.  The only atomic is an integer atomicMin on the
 // 64-bit (cost, k) key, which is order independent.
 #include <climits>
+#include <type_traits>
 
 #include "mppi_internal.h"
 
@@ -44,16 +45,15 @@ __device__ __forceinline__ void store_eps(float* p, const float* z) {
 }
 
 // Per-thread asynchronous copy of one noise element group (4m bytes) into shared memory
-// (LDGSTS; Ampere+ cp.async, non-blocking: no register is tied to the load).
+// (LDGSTS: cp.async, non-blocking, no register tied to the load).  dst: shared-window address.
 template <int M>
-__device__ __forceinline__ void cp_async_eps(float* smem_dst, const float* gsrc) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+__device__ __forceinline__ void cp_async_eps(unsigned dst, const float* gsrc) {
     if constexpr (M == 4) {
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(gsrc) : "memory");
     } else if constexpr (M == 2) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(gsrc) : "memory");
     } else {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(gsrc) : "memory");
     }
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
@@ -61,15 +61,14 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <int M>
-__device__ __forceinline__ void load_smem_eps(const float* p, float* e) {
+__device__ __forceinline__ void load_shared_eps(unsigned src, float* e) {
     if constexpr (M == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(p);
-        e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                     : "=f"(e[0]), "=f"(e[1]), "=f"(e[2]), "=f"(e[3]) : "r"(src) : "memory");
     } else if constexpr (M == 2) {
-        const float2 v = *reinterpret_cast<const float2*>(p);
-        e[0] = v.x; e[1] = v.y;
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(e[0]), "=f"(e[1]) : "r"(src) : "memory");
     } else {
-        e[0] = *p;
+        asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(e[0]) : "r"(src) : "memory");
     }
 }
 
@@ -159,17 +158,14 @@ struct RolloutArgs {
 // the same polynomial in eps with the per-t constants staged in shared memory.
 // eps[t][k] reaches the thread through a kEpsStages-deep shared-memory ring filled by per-thread
 // cp.async two steps ahead, so the HBM latency is hidden without tying up registers.
-template <class Plant, bool DIAG>
+template <class Plant, bool DIAG, int NP>
 __global__ void __launch_bounds__(kRolloutThreads, 8)
     rollout_kernel(const RolloutArgs<typename Plant::Params> a) {
     constexpr int M = Plant::M;
     extern __shared__ float4 smem4[];
     float4* sObs = smem4;
-    float4* sU = smem4 + a.n_obs_pairs;   // U_t, zero padded to 4         [T]
-    float4* sB = sU + a.T;                // DIAG: s_i (R U_t)_i; else (R U_t)_i   [T]
-    float* sK = reinterpret_cast<float*>(sB + a.T);   // U_t'R U_t / 2   [T]
-    float* sRing = reinterpret_cast<float*>(smem4 + a.n_obs_pairs + 2 * a.T) +
-                   ((a.T + 3) & ~3);                  // eps ring [kEpsStages][blockDim][M]
+    StepRec* sRec = reinterpret_cast<StepRec*>(smem4 + a.n_obs_pairs);   // per-t constants [T]
+    float* sRing = reinterpret_cast<float*>(sRec + a.T);               // eps ring [2][blockDim][M]
     const int tid = threadIdx.x;
     for (int i = tid; i < a.n_obs_pairs; i += blockDim.x) sObs[i] = a.obs[i];
     for (int t = tid; t < a.T; t += blockDim.x) {
@@ -185,9 +181,11 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
             kk = fmaf(u[i], ru, kk);
             bq[i] = DIAG ? a.sd[i] * ru : ru;
         }
-        sU[t] = make_float4(u[0], u[1], u[2], u[3]);
-        sB[t] = make_float4(bq[0], bq[1], bq[2], bq[3]);
-        sK[t] = 0.5f * kk;
+        StepRec r;
+        r.u = make_float4(u[0], u[1], u[2], u[3]);
+        r.b = make_float4(bq[0], bq[1], bq[2], bq[3]);
+        r.k = make_float4(0.5f * kk, 0.0f, 0.0f, 0.0f);
+        sRec[t] = r;
     }
     __syncthreads();
 
@@ -199,13 +197,13 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
         const ObstacleView ob{sObs, a.n_obs_pairs};
         const size_t row = (size_t)a.K_loc * M;
         float S = 0.0f;
-        auto one_step = [&](int t, const float* e) {
-            const float4 u4 = sU[t];
-            const float4 b4 = sB[t];
+        auto one_step = [&](const StepRec* rec, const float* e) {
+            const float4 u4 = rec->u;
+            const float4 b4 = rec->b;
             const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
             const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
             float v[M];
-            float is = sK[t];
+            float is = rec->k.x;
             if (DIAG) {
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
@@ -231,29 +229,26 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
                 }
                 is = fmaf(a.c1, duRdu, uRdu + is);
             }
-            const float q = st.step(v, a.dt, a.P, ob);                 // x_{t+1}, q(x_{t+1})
+            const float q = st.template step<NP>(v, a.dt, a.P, ob);    // x_{t+1}, q(x_{t+1})
             S += q + is;                                               // S~ += q~
         };
-        const float* ep = a.eps + (size_t)k * M;
-        float* ring = sRing + tid * M;                                 // slot stride: blockDim * M
-        const int slot_stride = blockDim.x * M;
-#pragma unroll
-        for (int j = 0; j < kEpsStages - 1; ++j) {                     // prologue: steps 0, 1
-            if (j < a.T) cp_async_eps<M>(ring + j * slot_stride, ep + (size_t)j * row);
+        // eps ring: two slots, the copy for step t+1 is issued before step t is computed
+        const float* gp = a.eps + (size_t)k * M;
+        const unsigned slot0 = (unsigned)__cvta_generic_to_shared(sRing + tid * M);
+        const unsigned slot_sum = 2u * slot0 + blockDim.x * M * (unsigned)sizeof(float);
+        unsigned cur = slot0;                                          // other slot = slot_sum - cur
+        cp_async_eps<M>(cur, gp);
+        cp_async_commit();
+        const StepRec* rec = sRec;
+        for (int t = 0; t < a.T; ++t, ++rec) {
+            gp += row;
+            if (t + 1 < a.T) cp_async_eps<M>(slot_sum - cur, gp);      // step t+1 in flight
             cp_async_commit();
-        }
-        int slot = 0;
-        for (int t = 0; t < a.T; ++t) {
-            const int ahead = t + kEpsStages - 1;
-            int fill = slot + kEpsStages - 1;
-            fill = fill >= kEpsStages ? fill - kEpsStages : fill;
-            if (ahead < a.T) cp_async_eps<M>(ring + fill * slot_stride, ep + (size_t)ahead * row);
-            cp_async_commit();
-            cp_async_wait<kEpsStages - 1>();                           // step t has landed
+            cp_async_wait<1>();                                        // step t has landed
             float e[M];
-            load_smem_eps<M>(ring + slot * slot_stride, e);
-            one_step(t, e);
-            slot = slot + 1 == kEpsStages ? 0 : slot + 1;
+            load_shared_eps<M>(cur, e);
+            one_step(rec, e);
+            cur = slot_sum - cur;
         }
         if (!isfinite(S)) S = a.penalty;
         a.costs[k] = S;
@@ -482,7 +477,7 @@ cudaError_t launch_noise(Ctx& c, uint64_t seed, uint64_t step, float* out, bool 
     return cudaGetLastError();
 }
 
-template <class Plant, bool DIAG>
+template <class Plant, bool DIAG, int NP>
 static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, const float* x0,
                                     const float* U, const float* eps, float* costs_out) {
     RolloutArgs<typename Plant::Params> a;
@@ -506,10 +501,9 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     }
     for (int i = 0; i < c.n && i < 16; ++i) a.x0[i] = x0[i];
     a.P = P;
-    const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * 2 * sizeof(float4) +
-                        (size_t)((c.T + 3) & ~3) * sizeof(float) +
-                        (size_t)kEpsStages * kRolloutThreads * Plant::M * sizeof(float);
-    auto kern = rollout_kernel<Plant, DIAG>;
+    const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
+                        (size_t)2 * kRolloutThreads * Plant::M * sizeof(float);
+    auto kern = rollout_kernel<Plant, DIAG, NP>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -521,11 +515,33 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     return cudaGetLastError();
 }
 
+// The quadrotor's obstacle loop is compiled for the context's exact pair count when it is at
+// most kMaxStaticPairs (diagonal L and R: every shipped configuration); other plants, general
+// covariances and larger forests use the runtime-count loop.
+template <class Plant, bool DIAG, int NP>
+static cudaError_t dispatch_np(Ctx& c, const typename Plant::Params& P, const float* x0,
+                               const float* U, const float* eps, float* costs_out) {
+    if constexpr (NP > kMaxStaticPairs) {
+        return launch_rollout_t<Plant, DIAG, -1>(c, P, x0, U, eps, costs_out);
+    } else {
+        if (c.n_obs_pairs == NP) return launch_rollout_t<Plant, DIAG, NP>(c, P, x0, U, eps, costs_out);
+        return dispatch_np<Plant, DIAG, NP + 1>(c, P, x0, U, eps, costs_out);
+    }
+}
+
+template <class Plant, bool DIAG>
+static cudaError_t launch_rollout_np(Ctx& c, const typename Plant::Params& P, const float* x0,
+                                     const float* U, const float* eps, float* costs_out) {
+    if constexpr (std::is_same<Plant, Quadrotor>::value && DIAG)
+        return dispatch_np<Plant, DIAG, 0>(c, P, x0, U, eps, costs_out);
+    return launch_rollout_t<Plant, DIAG, -1>(c, P, x0, U, eps, costs_out);
+}
+
 template <class Plant>
 static cudaError_t launch_rollout_p(Ctx& c, const typename Plant::Params& P, const float* x0,
                                     const float* U, const float* eps, float* costs_out) {
-    return c.diag ? launch_rollout_t<Plant, true>(c, P, x0, U, eps, costs_out)
-                  : launch_rollout_t<Plant, false>(c, P, x0, U, eps, costs_out);
+    return c.diag ? launch_rollout_np<Plant, true>(c, P, x0, U, eps, costs_out)
+                  : launch_rollout_np<Plant, false>(c, P, x0, U, eps, costs_out);
 }
 
 cudaError_t launch_rollout(Ctx& c, const float* x0, const float* U, const float* eps,
@@ -571,6 +587,15 @@ cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key) {
     }
     c.last_launches++;
     return cudaGetLastError();
+}
+
+int wsum_blocks_per_sm(int m) {
+    int n = 0;
+    cudaError_t e = cudaErrorInvalidValue;
+    if (m == 1) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wsum_kernel<1>, kWsumThreads, 0);
+    if (m == 2) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wsum_kernel<2>, kWsumThreads, 0);
+    if (m == 4) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wsum_kernel<4>, kWsumThreads, 0);
+    return (e == cudaSuccess && n > 0) ? n : 1;
 }
 
 cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* U) {
@@ -622,7 +647,7 @@ static float host_step_t(const Ctx& c, const typename Plant::Params& P, float* x
     for (int i = 0; i < c.n && i < 16; ++i) xin[i] = x[i];
     st.load(xin, crashed ? *crashed : 0);
     const ObstacleView ob{c.obs_host.data(), c.n_obs_pairs};
-    const float q = st.step(u, c.dt, P, ob);
+    const float q = st.template step<-1>(u, c.dt, P, ob);
     float xo[16] = {0};
     st.store(xo);
     for (int i = 0; i < c.n; ++i) x[i] = xo[i];

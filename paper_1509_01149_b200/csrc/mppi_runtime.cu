@@ -339,12 +339,14 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
     if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaGetDevice (no CUDA device?)"); }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-    // weighted-noise reduction grid: ~8 resident 256-thread CTAs per SM over (chunks x t-tiles)
+    // weighted-noise reduction grid (n_chunks x t-tiles CTAs): a whole number of waves of the
+    // resident CTA slots (just under, so the last wave is full), about 4 waves, at least 256
+    // float4 columns per chunk
     const int64_t ncols = K_loc * m / 4;
     const int ttiles = (T + kWsumTT - 1) / kWsumTT;
-    int64_t target = (int64_t)sms * 8;
-    int64_t nch = (target + ttiles - 1) / ttiles;
+    const int64_t slots = (int64_t)sms * wsum_blocks_per_sm(m);
     const int64_t max_ch = (ncols + kWsumThreads - 1) / kWsumThreads;
+    int64_t nch = (4 * slots) / ttiles;
     if (nch > max_ch) nch = max_ch;
     if (nch < 1) nch = 1;
     c.cols_per_chunk = (ncols + nch - 1) / nch;
