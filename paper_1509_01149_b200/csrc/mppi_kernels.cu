@@ -147,6 +147,7 @@ struct RolloutArgs {
     float ad[4];            // diagonal path: a_i = (1 - 1/nu)/2 R_ii s_i^2
     float x0[16];
     PP P;
+    float4 obs_k[kMaxStaticPairs];  // negated obstacle pairs again, in the parameter constant bank
 };
 
 // One sample per thread.  Per step t:
@@ -160,7 +161,7 @@ struct RolloutArgs {
 // cp.async two steps ahead, so the HBM latency is hidden without tying up registers.
 template <class Plant, bool DIAG, int NP>
 __global__ void __launch_bounds__(kRolloutThreads, 8)
-    rollout_kernel(const RolloutArgs<typename Plant::Params> a) {
+    rollout_kernel(const __grid_constant__ RolloutArgs<typename Plant::Params> a) {
     constexpr int M = Plant::M;
     extern __shared__ float4 smem4[];
     float4* sObs = smem4;
@@ -194,10 +195,12 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
     if (k < a.K_loc) {
         Plant st;
         st.load(a.x0, 0);
-        const ObstacleView ob{sObs, a.n_obs_pairs};
+        // compile-time pair count: read the forest from the kernel-parameter constant bank
+        // (uniform-register operands, no per-thread registers); else shared memory
+        const ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
         const size_t row = (size_t)a.K_loc * M;
         float S = 0.0f;
-        auto one_step = [&](const StepRec* rec, const float* e) {
+        auto one_step = [&](const StepRec* rec, const float* e, bool first) {
             const float4 u4 = rec->u;
             const float4 b4 = rec->b;
             const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
@@ -229,7 +232,12 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
                 }
                 is = fmaf(a.c1, duRdu, uRdu + is);
             }
-            const float q = st.template step<NP>(v, a.dt, a.P, ob);    // x_{t+1}, q(x_{t+1})
+            // rotated step: q(x_t) (the cost of step t-1, 0 at t = 0) and F(x_t, v_t) only need
+            // x_t, so they share one basic block; then x_{t+1} = x_t + F dt
+            const float q = st.template state_cost<NP>(first, a.P, ob);
+            float xd[Plant::N];
+            if (st.deriv_fast(v, a.P, xd)) st.deriv_accurate(v, a.P, xd);   // |angle| > 105615: rare
+            st.update(xd, a.dt);
             S += q + is;                                               // S~ += q~
         };
         // eps ring: two slots, the copy for step t+1 is issued before step t is computed
@@ -247,9 +255,10 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
             cp_async_wait<1>();                                        // step t has landed
             float e[M];
             load_shared_eps<M>(cur, e);
-            one_step(rec, e);
+            one_step(rec, e, t == 0);
             cur = slot_sum - cur;
         }
+        S += st.template state_cost<NP>(false, a.P, ob);              // q(x_T), step T-1
         if (!isfinite(S)) S = a.penalty;
         a.costs[k] = S;
         if (a.costs_out) a.costs_out[k] = S;
@@ -501,6 +510,8 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     }
     for (int i = 0; i < c.n && i < 16; ++i) a.x0[i] = x0[i];
     a.P = P;
+    for (int i = 0; i < kMaxStaticPairs; ++i)
+        a.obs_k[i] = i < c.n_obs_pairs ? c.obs_host[i] : make_float4(-1e15f, -1e15f, -1e15f, -1e15f);
     const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
                         (size_t)2 * kRolloutThreads * Plant::M * sizeof(float);
     auto kern = rollout_kernel<Plant, DIAG, NP>;
@@ -647,7 +658,11 @@ static float host_step_t(const Ctx& c, const typename Plant::Params& P, float* x
     for (int i = 0; i < c.n && i < 16; ++i) xin[i] = x[i];
     st.load(xin, crashed ? *crashed : 0);
     const ObstacleView ob{c.obs_host.data(), c.n_obs_pairs};
-    const float q = st.template step<-1>(u, c.dt, P, ob);
+    float xd[Plant::N];
+    st.template state_cost<-1>(true, P, ob);   // cart-pole: sin/cos of the current angle
+    st.deriv_accurate(u, P, xd);
+    st.update(xd, c.dt);
+    const float q = st.template state_cost<-1>(false, P, ob);
     float xo[16] = {0};
     st.store(xo);
     for (int i = 0; i < c.n; ++i) x[i] = xo[i];
