@@ -250,6 +250,12 @@ mppi_status_t mppi_set_stream(mppi_ctx* ctx, void* cuda_stream);
 mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed,
                             uint64_t step, const float* noise);
 
+/* mppi_use_graph — mppi_optimize replays the step as one CUDA graph (default: enabled): built on
+ * the first call of each noise mode, later calls only update the kernel-node arguments (x0,
+ * seed, step, U, noise).  Results are identical to direct launches.  While per-kernel profiling
+ * is enabled (mppi_profile_enable) kernels are launched directly. */
+mppi_status_t mppi_use_graph(mppi_ctx* ctx, int32_t enable);
+
 /* mppi_optimize_host — the same step end to end from HOST buffers: copies x0 and U in,
  * runs mppi_optimize on the context's device copy of U, copies the updated U back.
  * SYNCHRONOUS (returns after U is in host memory).  U: HOST float [T][m] in/out. */

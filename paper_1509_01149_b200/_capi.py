@@ -91,7 +91,7 @@ class kernel_times_t(C.Structure):
 
 KERNEL_NAMES = ["noise", "rollout", "wsum", "finalize", "shift"]
 
-EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize",
+EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize", "mppi_use_graph",
            "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_apply",
            "mppi_shift", "mppi_noise", "mppi_plant_step", "mppi_get_stats",
            "mppi_last_launch_count", "mppi_profile_enable", "mppi_profile_read", "mppi_last_error", "mppi_status_string", "mppi_abi_version"]
@@ -123,6 +123,8 @@ def lib():
     L.mppi_set_stream.restype = st
     L.mppi_optimize.argtypes = [vp, fp, vp, C.c_uint64, C.c_uint64, vp]
     L.mppi_optimize.restype = st
+    L.mppi_use_graph.argtypes = [vp, C.c_int32]
+    L.mppi_use_graph.restype = st
     L.mppi_optimize_host.argtypes = [vp, fp, fp, C.c_uint64, C.c_uint64]
     L.mppi_optimize_host.restype = st
     L.mppi_rollout_costs.argtypes = [vp, fp, vp, C.c_uint64, C.c_uint64, vp, vp, vp]

@@ -34,6 +34,24 @@ union PlantParamsU {
     LinearParams linear;
 };
 
+// One kernel launch: the kernel takes a single by-value parameter struct, copied here so the
+// launch can go to the stream directly or become (or update) a node of the context's CUDA graph.
+struct KLaunch {
+    const void* func = nullptr;
+    dim3 grid, block;
+    size_t smem = 0;
+    int kind = 0;
+    alignas(16) unsigned char args[2048];
+    void* argp[1];
+};
+
+struct GraphState {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<cudaGraphNode_t> nodes;   // kernel nodes in launch order
+    std::vector<const void*> funcs;
+};
+
 // Device-side per-step results readable by mppi_get_stats.
 struct DeviceStats {
     long long min_key;
@@ -76,7 +94,16 @@ struct Ctx {
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
     double prof_ms[MPPI_KERNEL_KINDS] = {0};
     int64_t prof_n[MPPI_KERNEL_KINDS] = {0};
+    // CUDA-graph replay of mppi_optimize (world == 1): [0] generated noise, [1] supplied noise
+    bool use_graph = true;
+    bool collect = false;                 // launchers append to `pending` instead of launching
+    std::vector<KLaunch> pending;
+    GraphState graphs[2];
 };
+
+// Launch (or collect, see Ctx::collect) one kernel whose single parameter is `args`.
+cudaError_t emit(Ctx& c, const void* func, dim3 grid, dim3 block, size_t smem, const void* args,
+                 size_t size, int kind);
 
 // Brackets one kernel launch with CUDA events when profiling is on.
 struct ProfScope {

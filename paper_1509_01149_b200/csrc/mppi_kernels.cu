@@ -13,6 +13,7 @@
 // reproducible run to run.  The only atomic is an integer atomicMin on the
 // 64-bit (cost, k) key, which is order independent.
 #include <climits>
+#include <cstring>
 #include <type_traits>
 
 #include "mppi_internal.h"
@@ -105,22 +106,37 @@ __device__ __forceinline__ float warp_sum(float v) {
 // Grid (ceil(K_loc/256), ceil(T/kNoiseTT)): each thread owns one sample k and kNoiseTT timesteps
 // (independent Philox calls, unrolled by two for ILP), so the per-thread setup is amortised.
 // Block (0,0) also resets the min key for the rollout that follows on the same stream.
+struct NoiseArgs {
+    float* eps;
+    int K_loc, T;
+    unsigned k_offset, step_lo, step_hi;
+    PhiloxKeys keys;
+    long long* key_reset;   // min key to reset (block (0,0)) or nullptr
+};
+
 template <int M>
-__global__ void __launch_bounds__(256) noise_kernel(float* __restrict__ eps, int K_loc, int T,
-                                                    unsigned k_offset, unsigned step_lo,
-                                                    unsigned step_hi, const PhiloxKeys keys,
-                                                    long long* key_reset) {
+__global__ void __launch_bounds__(256) noise_kernel(const NoiseArgs a) {
     const int k = blockIdx.x * 256 + threadIdx.x;
     const int t0 = blockIdx.y * kNoiseTT;
-    if (key_reset && k == 0 && t0 == 0) *key_reset = LLONG_MAX;
-    if (k >= K_loc) return;
-    const unsigned kg = k_offset + (unsigned)k;
-    const int t1 = min(t0 + kNoiseTT, T);
-    const size_t row = (size_t)K_loc * M;
-    float* p = eps + ((size_t)t0 * K_loc + k) * M;
-#pragma unroll 2
-    for (int t = t0; t < t1; ++t, p += row) {
-        const uint4 w = philox4x32_10_dev(kg, (unsigned)t, step_lo, step_hi, keys);
+    if (a.key_reset && k == 0 && t0 == 0) *a.key_reset = LLONG_MAX;
+    if (k >= a.K_loc) return;
+    const unsigned kg = a.k_offset + (unsigned)k;
+    const int t1 = min(t0 + kNoiseTT, a.T);
+    const size_t row = (size_t)a.K_loc * M;
+    float* p = a.eps + ((size_t)t0 * a.K_loc + k) * M;
+    int t = t0;
+    // two timesteps per iteration: their Box-Muller transforms run as packed FP32x2 (each lane
+    // of FFMA2/FMUL2/FADD2 is the same IEEE operation as the scalar sequence)
+    for (; t + 1 < t1; t += 2, p += 2 * row) {
+        const uint4 wa = philox4x32_10_dev(kg, (unsigned)t, a.step_lo, a.step_hi, a.keys);
+        const uint4 wb = philox4x32_10_dev(kg, (unsigned)(t + 1), a.step_lo, a.step_hi, a.keys);
+        float za[M], zb[M];
+        bm32_normals_x2<M>(wa, wb, za, zb);
+        store_eps<M>(p, za);
+        store_eps<M>(p + row, zb);
+    }
+    if (t < t1) {
+        const uint4 w = philox4x32_10_dev(kg, (unsigned)t, a.step_lo, a.step_hi, a.keys);
         float z[M];
         bm32_normals<M>(w, z);
         store_eps<M>(p, z);
@@ -416,7 +432,16 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeArgs a) {
 }
 
 // ------------------------------------------------------------------------------ K5 shift
-__global__ void __launch_bounds__(1024) shift_kernel(float* U, int T, int M, float4 u_init) {
+struct ShiftArgs {
+    float* U;
+    int T, M;
+    float4 u_init;
+};
+
+__global__ void __launch_bounds__(1024) shift_kernel(const ShiftArgs a) {
+    float* U = a.U;
+    const int T = a.T, M = a.M;
+    const float4 u_init = a.u_init;
     extern __shared__ float sU[];
     const int TM = T * M;
     for (int o = threadIdx.x; o < TM; o += blockDim.x) sU[o] = U[o];
@@ -443,6 +468,26 @@ static cudaEvent_t take_event(Ctx& c) {
     cudaEvent_t e = nullptr;
     cudaEventCreate(&e);
     return e;
+}
+
+cudaError_t emit(Ctx& c, const void* func, dim3 grid, dim3 block, size_t smem, const void* args,
+                 size_t size, int kind) {
+    if (size > sizeof(KLaunch::args)) return cudaErrorInvalidValue;
+    c.last_launches++;
+    if (c.collect) {
+        c.pending.emplace_back();
+        KLaunch& L = c.pending.back();
+        L.func = func;
+        L.grid = grid;
+        L.block = block;
+        L.smem = smem;
+        L.kind = kind;
+        memcpy(L.args, args, size);
+        return cudaSuccess;
+    }
+    ProfScope prof(c, kind);
+    void* argp[1] = {const_cast<void*>(args)};
+    return cudaLaunchKernel(func, grid, block, argp, smem, c.stream);
 }
 
 ProfScope::ProfScope(Ctx& c_, int kind_) : c(c_), kind(kind_) {
@@ -473,17 +518,19 @@ static PhiloxKeys philox_key_schedule(uint64_t seed) {
 cudaError_t launch_noise(Ctx& c, uint64_t seed, uint64_t step, float* out, bool reset_key) {
     const PhiloxKeys keys = philox_key_schedule(seed);
     const dim3 grid((unsigned)((c.K_loc + 255) / 256), (unsigned)((c.T + kNoiseTT - 1) / kNoiseTT));
-    ProfScope prof(c, MPPI_KERNEL_NOISE);
-    long long* kr = reset_key ? reinterpret_cast<long long*>(&c.d_stats->min_key) : nullptr;
-    const unsigned ko = (unsigned)c.k_offset, slo = (unsigned)step, shi = (unsigned)(step >> 32);
-    switch (c.m) {
-        case 1: noise_kernel<1><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, c.T, ko, slo, shi, keys, kr); break;
-        case 2: noise_kernel<2><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, c.T, ko, slo, shi, keys, kr); break;
-        case 4: noise_kernel<4><<<grid, 256, 0, c.stream>>>(out, (int)c.K_loc, c.T, ko, slo, shi, keys, kr); break;
-        default: return cudaErrorInvalidValue;
-    }
-    c.last_launches++;
-    return cudaGetLastError();
+    NoiseArgs a;
+    a.eps = out;
+    a.K_loc = (int)c.K_loc;
+    a.T = c.T;
+    a.k_offset = (unsigned)c.k_offset;
+    a.step_lo = (unsigned)step;
+    a.step_hi = (unsigned)(step >> 32);
+    a.keys = keys;
+    a.key_reset = reset_key ? reinterpret_cast<long long*>(&c.d_stats->min_key) : nullptr;
+    const void* f = c.m == 1 ? (const void*)noise_kernel<1> : c.m == 2 ? (const void*)noise_kernel<2>
+                  : c.m == 4 ? (const void*)noise_kernel<4> : nullptr;
+    if (!f) return cudaErrorInvalidValue;
+    return emit(c, f, grid, dim3(256), 0, &a, sizeof(a), MPPI_KERNEL_NOISE);
 }
 
 template <class Plant, bool DIAG, int NP>
@@ -520,10 +567,8 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
         if (e != cudaSuccess) return e;
     }
     const unsigned grid = (unsigned)((c.K_loc + kRolloutThreads - 1) / kRolloutThreads);
-    ProfScope prof(c, MPPI_KERNEL_ROLLOUT);
-    kern<<<grid, kRolloutThreads, smem, c.stream>>>(a);
-    c.last_launches++;
-    return cudaGetLastError();
+    return emit(c, (const void*)kern, dim3(grid), dim3(kRolloutThreads), smem, &a, sizeof(a),
+                MPPI_KERNEL_ROLLOUT);
 }
 
 // The quadrotor's obstacle loop is compiled for the context's exact pair count when it is at
@@ -589,15 +634,10 @@ cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key) {
     a.cols_per_chunk = c.cols_per_chunk;
     a.lambda = c.lambda;
     const dim3 grid((unsigned)c.n_chunks, (unsigned)((c.T + kWsumTT - 1) / kWsumTT));
-    ProfScope prof(c, MPPI_KERNEL_WSUM);
-    switch (c.m) {
-        case 1: wsum_kernel<1><<<grid, kWsumThreads, 0, c.stream>>>(a); break;
-        case 2: wsum_kernel<2><<<grid, kWsumThreads, 0, c.stream>>>(a); break;
-        case 4: wsum_kernel<4><<<grid, kWsumThreads, 0, c.stream>>>(a); break;
-        default: return cudaErrorInvalidValue;
-    }
-    c.last_launches++;
-    return cudaGetLastError();
+    const void* f = c.m == 1 ? (const void*)wsum_kernel<1> : c.m == 2 ? (const void*)wsum_kernel<2>
+                  : c.m == 4 ? (const void*)wsum_kernel<4> : nullptr;
+    if (!f) return cudaErrorInvalidValue;
+    return emit(c, f, grid, dim3(kWsumThreads), 0, &a, sizeof(a), MPPI_KERNEL_WSUM);
 }
 
 int wsum_blocks_per_sm(int m) {
@@ -627,10 +667,8 @@ cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* 
         if (e != cudaSuccess) return e;
     }
     const int threads = c.T * c.m >= 1024 ? 1024 : ((c.T * c.m + 31) / 32) * 32;
-    ProfScope prof(c, MPPI_KERNEL_FINALIZE);
-    finalize_kernel<<<1, threads, smem, c.stream>>>(a);
-    c.last_launches++;
-    return cudaGetLastError();
+    return emit(c, (const void*)finalize_kernel, dim3(1), dim3(threads), smem, &a, sizeof(a),
+                MPPI_KERNEL_FINALIZE);
 }
 
 cudaError_t launch_shift(Ctx& c, float* U, const float* u_init) {
@@ -643,10 +681,12 @@ cudaError_t launch_shift(Ctx& c, float* U, const float* u_init) {
         if (e != cudaSuccess) return e;
     }
     const int threads = c.T * c.m >= 1024 ? 1024 : ((c.T * c.m + 31) / 32) * 32;
-    ProfScope prof(c, MPPI_KERNEL_SHIFT);
-    shift_kernel<<<1, threads, smem, c.stream>>>(U, c.T, c.m, ui);
-    c.last_launches++;
-    return cudaGetLastError();
+    ShiftArgs a;
+    a.U = U;
+    a.T = c.T;
+    a.M = c.m;
+    a.u_init = ui;
+    return emit(c, (const void*)shift_kernel, dim3(1), dim3(threads), smem, &a, sizeof(a), MPPI_KERNEL_SHIFT);
 }
 
 // ------------------------------------------------------------------------------ host plant step

@@ -181,7 +181,19 @@ mppi_status_t digest_params(Ctx& c, const mppi_dynamics_t* d, const mppi_cost_t*
     }
 }
 
+void free_graphs(Ctx& c) {
+    for (GraphState& G : c.graphs) {
+        if (G.exec) cudaGraphExecDestroy(G.exec);
+        if (G.graph) cudaGraphDestroy(G.graph);
+        G.exec = nullptr;
+        G.graph = nullptr;
+        G.nodes.clear();
+        G.funcs.clear();
+    }
+}
+
 void free_ctx(Ctx& c) {
+    free_graphs(c);
     for (auto& p : c.ev_pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
     for (auto e : c.ev_pool) cudaEventDestroy(e);
     c.ev_pending.clear();
@@ -414,11 +426,83 @@ mppi_status_t mppi_set_stream(mppi_ctx* ctx, void* cuda_stream) {
     return MPPI_OK;
 }
 
+static cudaKernelNodeParams node_params(KLaunch& L) {
+    cudaKernelNodeParams p = {};
+    p.func = const_cast<void*>(L.func);
+    p.gridDim = L.grid;
+    p.blockDim = L.block;
+    p.sharedMemBytes = (unsigned)L.smem;
+    L.argp[0] = L.args;
+    p.kernelParams = L.argp;
+    p.extra = nullptr;
+    return p;
+}
+
+// mppi_optimize through a CUDA graph: the launchers collect their launches (same arguments as
+// the direct path), the graph is built once per context and noise mode, later calls only update
+// the kernel-node parameters (x0, seed, step, U and noise pointers) and replay it.
+static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t seed, uint64_t step,
+                                    const float* noise) {
+    if (!x0 || !U) return fail(MPPI_ERR_INVALID_ARG, "x0 and U must be non-NULL");
+    if (!all_finite(x0, c.n)) return fail(MPPI_ERR_INVALID_ARG, "x0 must be finite");
+    if (mppi_status_t s = sticky_check(c)) return s;
+    c.last_launches = 0;
+    c.pending.clear();
+    c.collect = true;
+    const float* eps = noise ? noise : c.d_eps;
+    cudaError_t e = cudaSuccess;
+    if (!noise) e = launch_noise(c, seed, step, c.d_eps, true);
+    if (e == cudaSuccess) e = launch_rollout(c, x0, U, eps, nullptr);
+    if (e == cudaSuccess) e = launch_wsum(c, eps, &c.d_stats->min_key);
+    if (e == cudaSuccess) e = launch_finalize(c, nullptr, nullptr, U);
+    c.collect = false;
+    if (e != cudaSuccess) return cuda_fail(e, "collecting the step's launches");
+    GraphState& G = c.graphs[noise ? 1 : 0];
+    bool same = G.exec && G.funcs.size() == c.pending.size();
+    for (size_t i = 0; same && i < c.pending.size(); ++i) same = G.funcs[i] == c.pending[i].func;
+    if (!same) {
+        if (G.exec) cudaGraphExecDestroy(G.exec);
+        if (G.graph) cudaGraphDestroy(G.graph);
+        G = GraphState();
+        MPPI_CUDA(cudaGraphCreate(&G.graph, 0), "cudaGraphCreate");
+        cudaGraphNode_t prev = nullptr;
+        if (noise) {   // supplied noise: the min key is reset by a copy node instead of K1
+            MPPI_CUDA(cudaGraphAddMemcpyNode1D(&prev, G.graph, nullptr, 0, &c.d_stats->min_key, c.d_key_init,
+                                               sizeof(long long), cudaMemcpyDeviceToDevice), "memcpy node");
+        }
+        for (KLaunch& L : c.pending) {
+            cudaKernelNodeParams p = node_params(L);
+            cudaGraphNode_t node;
+            MPPI_CUDA(cudaGraphAddKernelNode(&node, G.graph, prev ? &prev : nullptr, prev ? 1 : 0, &p),
+                      "cudaGraphAddKernelNode");
+            G.nodes.push_back(node);
+            G.funcs.push_back(L.func);
+            prev = node;
+        }
+        MPPI_CUDA(cudaGraphInstantiate(&G.exec, G.graph, 0), "cudaGraphInstantiate");
+    } else {
+        for (size_t i = 0; i < c.pending.size(); ++i) {
+            cudaKernelNodeParams p = node_params(c.pending[i]);
+            MPPI_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, G.nodes[i], &p), "graph node update");
+        }
+    }
+    MPPI_CUDA(cudaGraphLaunch(G.exec, c.stream), "cudaGraphLaunch");
+    c.last_eps = eps;
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_use_graph(mppi_ctx* ctx, int32_t enable) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    ctx->c.use_graph = enable != 0;
+    return MPPI_OK;
+}
+
 mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed, uint64_t step,
                             const float* noise) {
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
     if (c.world != 1) return fail(MPPI_ERR_UNSUPPORTED, "mppi_optimize needs world == 1; use the split-phase calls");
+    if (c.use_graph && !c.prof) return optimize_graph(c, x0, U, seed, step, noise);
     c.last_launches = 0;
     const float* eps = nullptr;
     if (mppi_status_t s = do_rollout(c, x0, U, seed, step, noise, nullptr, &eps)) return s;

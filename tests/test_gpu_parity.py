@@ -357,3 +357,27 @@ def test_full_size_c5_sampled(oracle):
     m.optimize(w.x0, U2, w.seed, 0)
     assert torch.equal(Us, U2) and torch.isfinite(U2).all()
     assert m.stats()["k_star"] == kk
+
+
+def test_graph_replay_matches_direct_launches():
+    """mppi_use_graph: the CUDA-graph replay of mppi_optimize gives the same bits as direct
+    launches, across seeds/steps, different U buffers and both noise modes."""
+    for cfg, K in (("C1", 256), ("C4", 4096)):
+        w = get(cfg)
+        g = from_workload(w, K=K)
+        d = from_workload(w, K=K)
+        d.use_graph(False)
+        for i, (seed, step) in enumerate([(1, 0), (1, 1), (7, 5), (1, 0)]):
+            Ug, Ud = cuda_u(w), cuda_u(w)
+            g.optimize(w.x0 + 0.01 * i, Ug, seed, step)
+            d.optimize(w.x0 + 0.01 * i, Ud, seed, step)
+            assert torch.equal(Ug, Ud), (cfg, seed, step)
+            assert g.stats() == d.stats()
+        eps = d.noise(3, 2)
+        Ug, Ud = cuda_u(w), cuda_u(w)
+        g.optimize(w.x0, Ug, 0, 0, noise=eps)
+        d.optimize(w.x0, Ud, 0, 0, noise=eps)
+        assert torch.equal(Ug, Ud)
+        Ug2 = cuda_u(w)
+        g.optimize(w.x0, Ug2, 3, 2)                 # generated mode again after supplied mode
+        assert torch.equal(Ug2, Ug)
