@@ -31,7 +31,7 @@ UNIT = "K*T/s"
 # 4 FFMA2 per thread, ncu sass counters / (K*T)); see DESIGN.md "Rollout FLOPs".  None -> not
 # yet measured for that plant (roofline falls back to the kernel's measured share only).
 ROLLOUT_FLOP_PER_SS = {"cartpole": None, "racecar": None,
-                       "quadrotor": 464.41}  # profiles/r1_ncu_full_c5_v5.txt (rollout v5)
+                       "quadrotor": 464.56}  # profiles/r1_ncu_full_c5_v7.txt (rollout v7, x2)
 
 SM_COUNT_B200 = 148
 FP32_LANES_PER_SM = 128

@@ -256,6 +256,15 @@ mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t s
  * is enabled (mppi_profile_enable) kernels are launched directly. */
 mppi_status_t mppi_use_graph(mppi_ctx* ctx, int32_t enable);
 
+typedef enum {
+    MPPI_OPTION_CUDA_GRAPH = 1,        /* same as mppi_use_graph (default 1) */
+    MPPI_OPTION_PACKED_SAMPLES = 2     /* quadrotor, diagonal Sigma and R: two samples per thread with
+                                          FP32x2 arithmetic (default 1); bitwise identical results */
+} mppi_option_t;
+
+/* mppi_set_option — execution options that never change results. */
+mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value);
+
 /* mppi_optimize_host — the same step end to end from HOST buffers: copies x0 and U in,
  * runs mppi_optimize on the context's device copy of U, copies the updated U back.
  * SYNCHRONOUS (returns after U is in host memory).  U: HOST float [T][m] in/out. */

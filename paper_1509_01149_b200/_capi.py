@@ -13,6 +13,7 @@ MPPI_OK, MPPI_ERR_INVALID_ARG, MPPI_ERR_NOT_SPD, MPPI_ERR_OOM, MPPI_ERR_CUDA, MP
     0, 1, 2, 3, 4, 6
 MPPI_PLANT_CARTPOLE, MPPI_PLANT_RACECAR, MPPI_PLANT_QUADROTOR, MPPI_PLANT_LINEAR = 1, 2, 3, 4
 MPPI_MAX_OBSTACLES = 4096
+MPPI_OPTION_CUDA_GRAPH, MPPI_OPTION_PACKED_SAMPLES = 1, 2
 
 
 class cartpole_dynamics_t(C.Structure):
@@ -91,7 +92,7 @@ class kernel_times_t(C.Structure):
 
 KERNEL_NAMES = ["noise", "rollout", "wsum", "finalize", "shift"]
 
-EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize", "mppi_use_graph",
+EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize", "mppi_use_graph", "mppi_set_option",
            "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_apply",
            "mppi_shift", "mppi_noise", "mppi_plant_step", "mppi_get_stats",
            "mppi_last_launch_count", "mppi_profile_enable", "mppi_profile_read", "mppi_last_error", "mppi_status_string", "mppi_abi_version"]
@@ -123,6 +124,8 @@ def lib():
     L.mppi_set_stream.restype = st
     L.mppi_optimize.argtypes = [vp, fp, vp, C.c_uint64, C.c_uint64, vp]
     L.mppi_optimize.restype = st
+    L.mppi_set_option.argtypes = [vp, C.c_int, C.c_int32]
+    L.mppi_set_option.restype = st
     L.mppi_use_graph.argtypes = [vp, C.c_int32]
     L.mppi_use_graph.restype = st
     L.mppi_optimize_host.argtypes = [vp, fp, fp, C.c_uint64, C.c_uint64]

@@ -67,6 +67,7 @@ struct Ctx {
     int rank = 0, world = 1;
     float dt = 0, lambda = 0, nu = 1, c1 = 0, penalty = 1e30f;
     bool diag = true;               // L and R both diagonal -> diagonal fast path
+    bool pack2 = true;              // quadrotor (diagonal): two samples per thread, FP32x2
     float sL[16] = {0};             // sqrt(nu) * chol(Sigma), fp32, row-major m x m
     float R[16] = {0};              // control cost, fp32
     float ad[4] = {0};              // diagonal path: (1 - 1/nu)/2 R_ii (sqrt(nu) L_ii)^2

@@ -291,6 +291,107 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
     }
 }
 
+// ------------------------------------------------------------------------------ K2 rollout, x2
+// Quadrotor with diagonal L and R: two adjacent samples per thread (k = 2j, 2j+1), every FP32
+// operation packed as FP32x2 (QuadrotorX2), the obstacle-pair loads shared by both samples.
+// Same per-step arithmetic and the same (cost, k) key as rollout_kernel.
+template <int NP>
+__global__ void __launch_bounds__(kRolloutThreads, 4)
+    rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
+    constexpr int M = 4;
+    extern __shared__ float4 smem4[];
+    float4* sObs = smem4;
+    StepRec* sRec = reinterpret_cast<StepRec*>(smem4 + a.n_obs_pairs);
+    float* sRing = reinterpret_cast<float*>(sRec + a.T);               // [2][blockDim][2 samples][4]
+    const int tid = threadIdx.x;
+    for (int i = tid; i < a.n_obs_pairs; i += blockDim.x) sObs[i] = a.obs[i];
+    for (int t = tid; t < a.T; t += blockDim.x) {
+        float u[4], bq[4];
+        float kk = 0.0f;
+#pragma unroll
+        for (int i = 0; i < M; ++i) u[i] = a.U[t * M + i];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            float ru = 0.0f;
+#pragma unroll
+            for (int j = 0; j < M; ++j) ru = fmaf(a.R[i * M + j], u[j], ru);
+            kk = fmaf(u[i], ru, kk);
+            bq[i] = a.sd[i] * ru;
+        }
+        StepRec r;
+        r.u = make_float4(u[0], u[1], u[2], u[3]);
+        r.b = make_float4(bq[0], bq[1], bq[2], bq[3]);
+        r.k = make_float4(0.5f * kk, 0.0f, 0.0f, 0.0f);
+        sRec[t] = r;
+    }
+    __syncthreads();
+
+    const int k = 2 * (blockIdx.x * blockDim.x + tid);                 // samples k, k+1
+    long long key = LLONG_MAX;
+    if (k < a.K_loc) {
+        QuadrotorX2 st;
+        st.load(a.x0);
+        const ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
+        const size_t row = (size_t)a.K_loc * M;
+        V2 S = vb(0.0f);
+        const float* gp = a.eps + (size_t)k * M;                       // 32 contiguous bytes
+        const unsigned slot0 = (unsigned)__cvta_generic_to_shared(sRing + tid * 2 * M);
+        const unsigned slot_sum = 2u * slot0 + blockDim.x * 2 * M * (unsigned)sizeof(float);
+        unsigned cur = slot0;
+        cp_async_eps<4>(cur, gp);
+        cp_async_eps<4>(cur + 16, gp + 4);
+        cp_async_commit();
+        const StepRec* rec = sRec;
+        for (int t = 0; t < a.T; ++t, ++rec) {
+            gp += row;
+            if (t + 1 < a.T) {
+                cp_async_eps<4>(slot_sum - cur, gp);
+                cp_async_eps<4>(slot_sum - cur + 16, gp + 4);
+            }
+            cp_async_commit();
+            cp_async_wait<1>();
+            float ea[4], eb[4];
+            load_shared_eps<4>(cur, ea);
+            load_shared_eps<4>(cur + 16, eb);
+            const float4 u4 = rec->u, b4 = rec->b;
+            const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+            V2 v[M];
+            V2 is = vb(rec->k.x);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const V2 e = vp(ea[i], eb[i]);
+                v[i] = fma2(vb(a.sd[i]), e, vb(uu[i]));                    // U_t + s_i eps_i
+                is = fma2(e, fma2(vb(a.ad[i]), e, vb(bb[i])), is);        // IS_t
+            }
+            const V2 q = st.template state_cost<NP>(t == 0, a.P, ob);    // q(x_t): step t-1
+            V2 xd[16];
+            if (st.deriv_fast(v, a.P, xd)) st.deriv_accurate(v, a.P, xd);
+            st.update(xd, a.dt);
+            S = S + (q + is);                                              // S~ += q~
+            cur = slot_sum - cur;
+        }
+        S = S + st.template state_cost<NP>(false, a.P, ob);               // q(x_T)
+        float sa = S.v.x, sb = S.v.y;
+        if (!isfinite(sa)) sa = a.penalty;
+        if (!isfinite(sb)) sb = a.penalty;
+        *reinterpret_cast<float2*>(a.costs + k) = make_float2(sa, sb);
+        if (a.costs_out) *reinterpret_cast<float2*>(a.costs_out + k) = make_float2(sa, sb);
+        const long long ka = cost_key(sa, a.k_offset + (unsigned)k);
+        const long long kb = cost_key(sb, a.k_offset + (unsigned)k + 1u);
+        key = ka < kb ? ka : kb;
+    }
+    key = warp_min_ll(key);
+    __shared__ long long wmin[kRolloutThreads / 32];
+    if ((tid & 31) == 0) wmin[tid >> 5] = key;
+    __syncthreads();
+    if (tid < 32) {
+        long long v = tid < (int)(blockDim.x >> 5) ? wmin[tid] : LLONG_MAX;
+        v = warp_min_ll(v);
+        if (tid == 0 && v != LLONG_MAX) atomicMin(a.min_key, v);
+    }
+}
+
 // ------------------------------------------------------------------------------ K3 weights + GEMV
 struct WsumArgs {
     const float* eps;           // [T][K_loc][M] viewed as [T][ncols] float4
@@ -533,7 +634,7 @@ cudaError_t launch_noise(Ctx& c, uint64_t seed, uint64_t step, float* out, bool 
     return emit(c, f, grid, dim3(256), 0, &a, sizeof(a), MPPI_KERNEL_NOISE);
 }
 
-template <class Plant, bool DIAG, int NP>
+template <class Plant, bool DIAG, int NP, bool X2 = false>
 static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, const float* x0,
                                     const float* U, const float* eps, float* costs_out) {
     RolloutArgs<typename Plant::Params> a;
@@ -559,14 +660,17 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     a.P = P;
     for (int i = 0; i < kMaxStaticPairs; ++i)
         a.obs_k[i] = i < c.n_obs_pairs ? c.obs_host[i] : make_float4(-1e15f, -1e15f, -1e15f, -1e15f);
+    const int spt = X2 ? 2 : 1;                                      // samples per thread
     const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
-                        (size_t)2 * kRolloutThreads * Plant::M * sizeof(float);
-    auto kern = rollout_kernel<Plant, DIAG, NP>;
+                        (size_t)2 * kRolloutThreads * spt * Plant::M * sizeof(float);
+    const void* kern;
+    if constexpr (X2) kern = (const void*)rollout_kernel_x2<NP>;
+    else kern = (const void*)rollout_kernel<Plant, DIAG, NP>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    const unsigned grid = (unsigned)((c.K_loc + kRolloutThreads - 1) / kRolloutThreads);
+    const unsigned grid = (unsigned)((c.K_loc / spt + kRolloutThreads - 1) / kRolloutThreads);
     return emit(c, (const void*)kern, dim3(grid), dim3(kRolloutThreads), smem, &a, sizeof(a),
                 MPPI_KERNEL_ROLLOUT);
 }
@@ -578,9 +682,13 @@ template <class Plant, bool DIAG, int NP>
 static cudaError_t dispatch_np(Ctx& c, const typename Plant::Params& P, const float* x0,
                                const float* U, const float* eps, float* costs_out) {
     if constexpr (NP > kMaxStaticPairs) {
+        if (c.pack2) return launch_rollout_t<Plant, DIAG, -1, true>(c, P, x0, U, eps, costs_out);
         return launch_rollout_t<Plant, DIAG, -1>(c, P, x0, U, eps, costs_out);
     } else {
-        if (c.n_obs_pairs == NP) return launch_rollout_t<Plant, DIAG, NP>(c, P, x0, U, eps, costs_out);
+        if (c.n_obs_pairs == NP) {
+            if (c.pack2) return launch_rollout_t<Plant, DIAG, NP, true>(c, P, x0, U, eps, costs_out);
+            return launch_rollout_t<Plant, DIAG, NP>(c, P, x0, U, eps, costs_out);
+        }
         return dispatch_np<Plant, DIAG, NP + 1>(c, P, x0, U, eps, costs_out);
     }
 }

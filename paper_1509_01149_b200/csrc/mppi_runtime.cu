@@ -497,6 +497,15 @@ mppi_status_t mppi_use_graph(mppi_ctx* ctx, int32_t enable) {
     return MPPI_OK;
 }
 
+mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    switch (option) {
+        case MPPI_OPTION_CUDA_GRAPH: ctx->c.use_graph = value != 0; return MPPI_OK;
+        case MPPI_OPTION_PACKED_SAMPLES: ctx->c.pack2 = value != 0; return MPPI_OK;
+        default: return fail(MPPI_ERR_INVALID_ARG, "unknown option %d", (int)option);
+    }
+}
+
 mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed, uint64_t step,
                             const float* noise) {
     if (mppi_status_t s = check_ctx(ctx)) return s;

@@ -101,6 +101,10 @@ class MPPI:
         """mppi_use_graph: replay mppi_optimize as one CUDA graph (default on)."""
         A.check(self.lib.mppi_use_graph(self.ctx, 1 if enable else 0))
 
+    def set_option(self, option, value):
+        """mppi_set_option (A.MPPI_OPTION_*): execution options that never change results."""
+        A.check(self.lib.mppi_set_option(self.ctx, option, int(value)))
+
     def optimize_host(self, x0, U, seed=0, step=0):
         """mppi_optimize_host: U is a host float32 array [T][m], updated in place (synchronous)."""
         if not (isinstance(U, np.ndarray) and U.dtype == np.float32 and U.flags.c_contiguous

@@ -381,3 +381,22 @@ def test_graph_replay_matches_direct_launches():
         Ug2 = cuda_u(w)
         g.optimize(w.x0, Ug2, 3, 2)                 # generated mode again after supplied mode
         assert torch.equal(Ug2, Ug)
+
+
+def test_packed_two_sample_rollout_is_bitwise_scalar():
+    """MPPI_OPTION_PACKED_SAMPLES: the quadrotor kernel with two samples per thread (FP32x2)
+    performs the same per-lane IEEE operations as the one-sample kernel: identical bits."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get("C4")
+    for K in (4096, 8192 + 4):
+        a = from_workload(w, K=K)
+        b = from_workload(w, K=K)
+        b.set_option(A.MPPI_OPTION_PACKED_SAMPLES, 0)
+        U = cuda_u(w)
+        ca, ka = a.rollout_costs(w.x0, U, 5, 3)
+        cb, kb = b.rollout_costs(w.x0, U, 5, 3)
+        assert torch.equal(ca, cb) and int(ka.item()) == int(kb.item())
+        Ua, Ub = cuda_u(w), cuda_u(w)
+        a.optimize(w.x0, Ua, 5, 3)
+        b.optimize(w.x0, Ub, 5, 3)
+        assert torch.equal(Ua, Ub)
