@@ -258,8 +258,9 @@ mppi_status_t mppi_use_graph(mppi_ctx* ctx, int32_t enable);
 
 typedef enum {
     MPPI_OPTION_CUDA_GRAPH = 1,        /* same as mppi_use_graph (default 1) */
-    MPPI_OPTION_PACKED_SAMPLES = 2     /* quadrotor, diagonal Sigma and R: two samples per thread with
-                                          FP32x2 arithmetic (default 1); bitwise identical results */
+    MPPI_OPTION_PACKED_SAMPLES = 2     /* quadrotor, diagonal Sigma and R, K_loc >= 65536: two samples
+                                          per thread with FP32x2 arithmetic (default 1); bitwise
+                                          identical results */
 } mppi_option_t;
 
 /* mppi_set_option — execution options that never change results. */

@@ -682,11 +682,11 @@ template <class Plant, bool DIAG, int NP>
 static cudaError_t dispatch_np(Ctx& c, const typename Plant::Params& P, const float* x0,
                                const float* U, const float* eps, float* costs_out) {
     if constexpr (NP > kMaxStaticPairs) {
-        if (c.pack2) return launch_rollout_t<Plant, DIAG, -1, true>(c, P, x0, U, eps, costs_out);
+        if (c.pack2 && c.K_loc >= kPackedMinK) return launch_rollout_t<Plant, DIAG, -1, true>(c, P, x0, U, eps, costs_out);
         return launch_rollout_t<Plant, DIAG, -1>(c, P, x0, U, eps, costs_out);
     } else {
         if (c.n_obs_pairs == NP) {
-            if (c.pack2) return launch_rollout_t<Plant, DIAG, NP, true>(c, P, x0, U, eps, costs_out);
+            if (c.pack2 && c.K_loc >= kPackedMinK) return launch_rollout_t<Plant, DIAG, NP, true>(c, P, x0, U, eps, costs_out);
             return launch_rollout_t<Plant, DIAG, NP>(c, P, x0, U, eps, costs_out);
         }
         return dispatch_np<Plant, DIAG, NP + 1>(c, P, x0, U, eps, costs_out);

@@ -388,7 +388,7 @@ def test_packed_two_sample_rollout_is_bitwise_scalar():
     performs the same per-lane IEEE operations as the one-sample kernel: identical bits."""
     from paper_1509_01149_b200 import _capi as A
     w = get("C4")
-    for K in (4096, 8192 + 4):
+    for K in (1 << 16, (1 << 17) + 4):
         a = from_workload(w, K=K)
         b = from_workload(w, K=K)
         b.set_option(A.MPPI_OPTION_PACKED_SAMPLES, 0)
