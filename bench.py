@@ -56,6 +56,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-probe", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-extra", action="store_true", help="skip the C3/C4/K-sweep/closed-loop extras")
     return p.parse_args()
 
 
@@ -223,6 +224,61 @@ def latency(cfg_name, iters=200, warm=20):
             "KT_per_s_at_p50": w.K * w.T / (q(dev, 0.5) * 1e-6)}
 
 
+# ----------------------------------------------------------------------------- other configs
+def throughput(cfg_name, K=None, steps=10, warm=3):
+    """K*T/s of one config on this GPU (graph replay, CUDA events around `steps` steps)."""
+    import torch
+    from mppi_inputs import get
+    from paper_1509_01149_b200 import from_workload
+    w = get(cfg_name)
+    m = from_workload(w, K=K or w.K)
+    U = torch.tensor(w.U0, device="cuda")
+    for i in range(warm):
+        m.optimize(w.x0, U, w.seed, i)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for i in range(steps):
+        m.optimize(w.x0, U, w.seed, warm + i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    m.close()
+    return {"plant": w.plant, "K": K or w.K, "T": w.T, "ms_per_step": ms,
+            "KT_per_s": (K or w.K) * w.T / (ms * 1e-3)}
+
+
+def closed_loop(cfg_name="C2"):
+    """Alg. 1 receding horizon through the public API: optimise (graph),
+    send u_0 (D2H), plant step on the host (mppi_plant_step), shift; per-step wall clock."""
+    import math as _m
+    import numpy as np
+    import torch
+    from mppi_inputs import get
+    from paper_1509_01149_b200 import from_workload
+    w = get(cfg_name)
+    m = from_workload(w)
+    U = torch.tensor(w.U0, device="cuda")
+    x = w.x0.copy()
+    crashed = 0
+    lat, qs = [], []
+    for step in range(w.steps):
+        t0 = time.perf_counter()
+        m.optimize(x, U, w.seed, step)
+        u0 = U[0].cpu().numpy()                       # "send to actuators" (PAPER.md:370)
+        lat.append((time.perf_counter() - t0) * 1e6)
+        x, q, crashed = m.plant_step(x, u0, crashed)  # environment step (noise-free)
+        m.shift(U, np.zeros(w.m, np.float32))         # PAPER.md:372-375, u_init = 0
+        qs.append(q)
+    torch.cuda.synchronize()
+    m.close()
+    srt = sorted(lat)
+    return {"config": cfg_name, "plant": w.plant, "K": w.K, "T": w.T, "nu": w.nu, "steps": w.steps,
+            "step_us_p50": srt[len(srt) // 2], "step_us_p99": srt[int(0.99 * (len(srt) - 1))],
+            "mean_q": float(np.mean(qs)), "final_1_plus_cos_theta": float(1 + _m.cos(x[2])),
+            "note": "optimize + u0 D2H per step (host wall clock); host plant step and shift excluded"}
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     args = parse_args()
@@ -372,6 +428,12 @@ def main():
     if not args.no_latency and world == 1:
         lat = {c: latency(c) for c in ("C1", "C2")}
 
+    extra = None
+    if not args.no_extra and world == 1:
+        extra = {"configs": {c: throughput(c) for c in ("C3", "C4")},
+                 "C5_sweep": [throughput("C5", K=1 << e, steps=5) for e in (16, 18, 20, 22)],
+                 "closed_loop": closed_loop("C2")}
+
     eps_bytes = 4 * w.T * K_loc * w.m
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -384,7 +446,7 @@ def main():
                    "l2": "inputs larger than L2 (noise %.1f GB per GPU per step)" % (eps_bytes / 1e9),
                    "parallelism": "K-sharded dp%d, NCCL MIN + SUM allreduce" % world},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-        "clocks": clk, "kernels": kern, "latency": lat,
+        "clocks": clk, "kernels": kern, "latency": lat, "extra": extra,
         "device": torch.cuda.get_device_name(local),
     }
     print(json.dumps(line), flush=True)

@@ -400,3 +400,30 @@ def test_packed_two_sample_rollout_is_bitwise_scalar():
         a.optimize(w.x0, Ua, 5, 3)
         b.optimize(w.x0, Ub, 5, 3)
         assert torch.equal(Ua, Ub)
+
+
+@pytest.mark.slow
+def test_closed_loop_c2_swings_up_like_the_oracle(oracle):
+    """Alg. 1 receding horizon through the public API at C2 (K=4096, T=100,
+    nu=1000): optimise, send u_0, host plant step (mppi_plant_step), shift.  The pole must swing
+    up and stay up like the fp64 oracle's closed loop; trajectories themselves
+    diverge chaotically between fp32 and fp64, so the behaviour is compared, not the states."""
+    w = get("C2")
+    m = from_workload(w)
+    U = cuda_u(w)
+    x = w.x0.copy()
+    c = 0
+    qs, up = [], []
+    for step in range(w.steps):
+        m.optimize(x, U, w.seed, step)
+        x, q, c = m.plant_step(x, U[0].cpu().numpy(), c)
+        m.shift(U, np.zeros(1, np.float32))
+        qs.append(q)
+        up.append(1 + math.cos(x[2]))
+    pb = oracle_problem(oracle, w)
+    xs, qo = oracle.closed_loop(pb, w.x0, w.U0, w.steps, w.seed, K=w.K)
+    up_o = 1 + np.cos(xs[1:, 2])
+    for series, cost in ((np.array(up), np.array(qs)), (up_o, qo)):
+        first = int(np.argmax(series < 0.05))
+        assert series.min() < 0.05 and first < 100
+        assert cost[-50:].mean() < 50.0
