@@ -297,6 +297,21 @@ mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, floa
  * order j = 0..i, U[t][i] = fl(U[t][i] + fl(d_i / eta)). */
 mppi_status_t mppi_apply(mppi_ctx* ctx, float* U, const float* buf);
 
+/* ---------------------------------------------------------------- path-integral estimate (NEXT-4) */
+
+/* mppi_feynman_kac — the Feynman-Kac path integral Psi(x0) = E_P[exp(-S(tau)/lambda)]
+ * (discrete form :78): K rollouts of this context's plant from x0 with U = 0 under
+ * the natural noise (the context must have nu == 1, so every importance-sampling term of q~
+ * vanishes and S~ = S = sum_t q(x_{t+1})), then, in a fixed-order reduction,
+ *   log Psi-hat = -S_min/lambda + log( (1/K) sum_k w_k ),  w_k = exp(-(S_k - S_min)/lambda),
+ *   se         = std_k(w_k) / (sqrt(K) mean_k(w_k))     (delta-method std. error of log Psi-hat).
+ * V(x0) = -lambda log Psi(x0) is the value function of PAPER.md:56.
+ *   x0  : HOST float [n];  seed, step : as mppi_optimize.
+ *   out : HOST double [3] = {log_psi, se_log_psi, s_min}.
+ * SYNCHRONOUS.  world == 1 only (else UNSUPPORTED); nu != 1 -> UNSUPPORTED. */
+mppi_status_t mppi_feynman_kac(mppi_ctx* ctx, const float* x0, uint64_t seed, uint64_t step,
+                               double* out);
+
 /* ---------------------------------------------------------------- helpers around the step */
 
 /* mppi_shift — Alg. 1: U_i = U_{i+1}, U_{T-1} = u_init.

@@ -85,7 +85,8 @@ struct Ctx {
     float* d_part = nullptr;        // [n_chunks][T*m]
     float* d_eta_part = nullptr;    // [n_chunks]
     DeviceStats* d_stats = nullptr;
-    float* d_U = nullptr;           // [T][m] for mppi_optimize_host
+    float* d_U = nullptr;           // [T][m] for mppi_optimize_host / mppi_feynman_kac
+    double* d_fk = nullptr;         // Feynman-Kac partial sums (lazy)
     float* h_U_pinned = nullptr;    // pinned staging for mppi_optimize_host
     int n_chunks = 1;
     int64_t cols_per_chunk = 0;     // float4 columns of a noise row per chunk
@@ -126,6 +127,7 @@ cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key);
 cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* U);
 cudaError_t launch_shift(Ctx& c, float* U, const float* u_init);
 int wsum_blocks_per_sm(int m);  // resident wsum CTAs per SM (occupancy API)
+cudaError_t launch_fk_reduce(Ctx& c, double* part, int nblk);   // Feynman-Kac partial sums
 
 // host plant step (mppi_runtime.cu uses it for mppi_plant_step)
 float host_plant_step(const Ctx& c, float* x, const float* u, int32_t* crashed);

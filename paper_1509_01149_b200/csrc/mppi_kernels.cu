@@ -532,6 +532,51 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeArgs a) {
     }
 }
 
+// ------------------------------------------------------------------------------ Feynman-Kac reduction
+// partial sums of w_k = exp(-(S_k - S_min)/lambda) and w_k^2 per CTA, fp64, fixed order
+struct FkArgs {
+    const float* costs;
+    const long long* key;
+    int K_loc;
+    float lambda;
+    double* part;   // [gridDim.x][2]
+};
+
+__global__ void __launch_bounds__(256) fk_reduce_kernel(const FkArgs a) {
+    const float smin = key_cost(*a.key);
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = blockIdx.x * 256 + threadIdx.x; k < a.K_loc; k += gridDim.x * 256) {
+        const double w = (double)expf(-__fdiv_rn(a.costs[k] - smin, a.lambda));
+        s1 += w;
+        s2 += w * w;
+    }
+    __shared__ double r1[256], r2[256];
+    r1[threadIdx.x] = s1;
+    r2[threadIdx.x] = s2;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            r1[threadIdx.x] += r1[threadIdx.x + o];
+            r2[threadIdx.x] += r2[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        a.part[2 * blockIdx.x] = r1[0];
+        a.part[2 * blockIdx.x + 1] = r2[0];
+    }
+}
+
+cudaError_t launch_fk_reduce(Ctx& c, double* part, int nblk) {
+    FkArgs a;
+    a.costs = c.d_costs;
+    a.key = &c.d_stats->min_key;
+    a.K_loc = (int)c.K_loc;
+    a.lambda = c.lambda;
+    a.part = part;
+    return emit(c, (const void*)fk_reduce_kernel, dim3(nblk), dim3(256), 0, &a, sizeof(a), MPPI_KERNEL_WSUM);
+}
+
 // ------------------------------------------------------------------------------ K5 shift
 struct ShiftArgs {
     float* U;

@@ -206,6 +206,7 @@ void free_ctx(Ctx& c) {
     cudaFree(c.d_eta_part);
     cudaFree(c.d_stats);
     cudaFree(c.d_U);
+    cudaFree(c.d_fk);
     if (c.h_U_pinned) cudaFreeHost(c.h_U_pinned);
 }
 
@@ -621,6 +622,41 @@ mppi_status_t mppi_get_stats(mppi_ctx* ctx, mppi_stats_t* out) {
 }
 
 int32_t mppi_last_launch_count(const mppi_ctx* ctx) { return ctx ? ctx->c.last_launches : 0; }
+
+mppi_status_t mppi_feynman_kac(mppi_ctx* ctx, const float* x0, uint64_t seed, uint64_t step, double* out) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
+    if (c.world != 1) return fail(MPPI_ERR_UNSUPPORTED, "mppi_feynman_kac needs world == 1");
+    if (c.nu != 1.0f) return fail(MPPI_ERR_UNSUPPORTED, "mppi_feynman_kac samples the uncontrolled "
+                                  "dynamics P: create the context with nu == 1");
+    c.last_launches = 0;
+    // U = 0 (uncontrolled dynamics) in the context's staging buffer
+    MPPI_CUDA(cudaMemsetAsync(c.d_U, 0, (size_t)c.T * c.m * sizeof(float), c.stream), "U = 0");
+    const float* eps = nullptr;
+    if (mppi_status_t s = do_rollout(c, x0, c.d_U, seed, step, nullptr, nullptr, &eps)) return s;
+    const int nblk = 148;
+    if (!c.d_fk) MPPI_CUDA(cudaMalloc((void**)&c.d_fk, 2 * nblk * sizeof(double)), "fk partials");
+    MPPI_CUDA(launch_fk_reduce(c, c.d_fk, nblk), "fk_reduce launch");
+    double part[2 * 148];
+    long long key = 0;
+    MPPI_CUDA(cudaMemcpyAsync(part, c.d_fk, sizeof(part), cudaMemcpyDeviceToHost, c.stream), "fk D2H");
+    MPPI_CUDA(cudaMemcpyAsync(&key, &c.d_stats->min_key, sizeof(key), cudaMemcpyDeviceToHost, c.stream), "key D2H");
+    MPPI_CUDA(cudaStreamSynchronize(c.stream), "stream sync");
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = 0; i < nblk; ++i) { s1 += part[2 * i]; s2 += part[2 * i + 1]; }
+    int b = (int)(key >> 32);
+    b = b >= 0 ? b : (b ^ 0x7fffffff);
+    float smin;
+    memcpy(&smin, &b, sizeof(smin));
+    const double K = (double)c.K_loc;
+    const double mean = s1 / K;
+    const double var = K > 1 ? (s2 / K - mean * mean) * K / (K - 1) : 0.0;
+    out[0] = -(double)smin / (double)c.lambda + log(mean);
+    out[1] = sqrt(var > 0 ? var : 0.0) / sqrt(K) / mean;
+    out[2] = (double)smin;
+    return MPPI_OK;
+}
 
 static mppi_status_t drain_profile(Ctx& c) {
     for (auto& p : c.ev_pending) {

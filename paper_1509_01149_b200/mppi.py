@@ -167,6 +167,15 @@ class MPPI:
         A.check(self.lib.mppi_noise(self.ctx, seed, step, _fptr(out)))
         return out
 
+    def feynman_kac(self, x0, seed=0, step=0):
+        """mppi_feynman_kac (PAPER.md:71-79): returns (log_psi, se_log_psi, s_min)."""
+        x = self._x0(x0)
+        out = np.zeros(3, np.float64)
+        self._sync_stream()
+        A.check(self.lib.mppi_feynman_kac(self.ctx, x.ctypes.data_as(C.POINTER(C.c_float)), seed, step,
+                                          out.ctypes.data_as(C.POINTER(C.c_double))))
+        return float(out[0]), float(out[1]), float(out[2])
+
     def plant_step(self, x, u, crashed=0):
         """mppi_plant_step: host fp32 Euler step; returns (x', q(x'), crashed')."""
         xs = _host_f32(x, self.n, "x").copy()
