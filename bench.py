@@ -279,6 +279,50 @@ def closed_loop(cfg_name="C2"):
             "note": "optimize + u0 D2H per step (host wall clock); host plant step and shift excluded"}
 
 
+def device_closed_loop(cfg_name="C2"):
+    """mppi_closed_loop: the whole receding-horizon loop as one CUDA graph (NEXT-2)."""
+    import math as _m
+    import torch
+    from mppi_inputs import get
+    from paper_1509_01149_b200 import from_workload
+    w = get(cfg_name)
+    m = from_workload(w)
+    x = torch.tensor(w.x0, device="cuda")
+    U = torch.tensor(w.U0, device="cuda")
+    m.closed_loop(x, U, 20, seed=w.seed, log=False)            # warm-up (graph build path)
+    x = torch.tensor(w.x0, device="cuda")
+    U = torch.tensor(w.U0, device="cuda")
+    t0 = time.perf_counter()
+    xl, ul, ql = m.closed_loop(x, U, w.steps, seed=w.seed)
+    el = time.perf_counter() - t0
+    xs = xl.cpu().numpy()
+    m.close()
+    return {"config": cfg_name, "steps": w.steps, "wall_us_per_step_incl_graph_build": el / w.steps * 1e6,
+            "mean_q": float(ql.mean().item()), "final_1_plus_cos_theta": float(1 + _m.cos(xs[-1, 2]))}
+
+
+def fig1_trend(nus=(1.0, 10.0, 100.0, 1000.0, 1500.0), Ks=(12, 100, 1000), seconds=10.0):
+    """PAPER.md:388-396 Fig. 1 (values unreadable; the trend is what can be compared): average
+    running cost of the cart-pole swing-up over 10 s at 50 Hz, 1 s horizon, for nu x K."""
+    import torch
+    from mppi_inputs.configs import cartpole
+    from paper_1509_01149_b200 import from_workload
+    steps = int(round(seconds / 0.02))
+    out = {}
+    for nu in nus:
+        row = {}
+        for K in Ks:
+            w = cartpole(K, 50, nu, steps=steps)
+            m = from_workload(w)
+            x = torch.tensor(w.x0, device="cuda")
+            U = torch.tensor(w.U0, device="cuda")
+            _, _, ql = m.closed_loop(x, U, steps, seed=1)
+            row[str(K)] = round(float(ql.mean().item()), 2)
+            m.close()
+        out[str(nu)] = row
+    return {"steps": steps, "T": 50, "mean_running_cost[nu][K]": out}
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     args = parse_args()
@@ -432,7 +476,9 @@ def main():
     if not args.no_extra and world == 1:
         extra = {"configs": {c: throughput(c) for c in ("C3", "C4")},
                  "C5_sweep": [throughput("C5", K=1 << e, steps=5) for e in (16, 18, 20, 22)],
-                 "closed_loop": closed_loop("C2")}
+                 "closed_loop": closed_loop("C2"),
+                 "device_closed_loop": device_closed_loop("C2"),
+                 "fig1_trend": fig1_trend()}
 
     eps_bytes = 4 * w.T * K_loc * w.m
     line = {

@@ -297,6 +297,25 @@ mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, floa
  * order j = 0..i, U[t][i] = fl(U[t][i] + fl(d_i / eta)). */
 mppi_status_t mppi_apply(mppi_ctx* ctx, float* U, const float* buf);
 
+/* ---------------------------------------------------------------- on-device MPC loop (NEXT-2) */
+
+/* mppi_closed_loop — Algorithm 1's while-loop for n_steps receding-horizon
+ * steps entirely on the device, as one CUDA graph: per step i
+ *   optimise U from the device state x (noise counter step0 + i),
+ *   send u_0 to the plant: x <- x + F(x, u_0) dt with this context's model, noise-free
+ *   (the plant's accurate path), then shift U (u_j = u_{j+1},
+ *   u_{T-1} = u_init).
+ *   x      : DEVICE float [n], the plant state, in/out.
+ *   U      : DEVICE float [T][m], in/out.
+ *   u_init : HOST float [m].
+ *   reset_crash : nonzero clears the device plant's crash flag (quadrotor) first.
+ *   x_log  : DEVICE float [n_steps + 1][n] (x_0 .. x_N) or NULL;  u_log: DEVICE [n_steps][m] (the
+ *            executed u_0) or NULL;  q_log: DEVICE [n_steps] (q(x_{i+1})) or NULL.
+ * SYNCHRONOUS (returns after the loop ran).  world == 1 and plant != LINEAR, else UNSUPPORTED. */
+mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed, uint64_t step0,
+                               int32_t n_steps, const float* u_init, int32_t reset_crash,
+                               float* x_log, float* u_log, float* q_log);
+
 /* ---------------------------------------------------------------- path-integral estimate (NEXT-4) */
 
 /* mppi_feynman_kac — the Feynman-Kac path integral Psi(x0) = E_P[exp(-S(tau)/lambda)]

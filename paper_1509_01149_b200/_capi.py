@@ -94,7 +94,7 @@ KERNEL_NAMES = ["noise", "rollout", "wsum", "finalize", "shift"]
 
 EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize", "mppi_use_graph", "mppi_set_option",
            "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_apply",
-           "mppi_shift", "mppi_noise", "mppi_feynman_kac", "mppi_plant_step", "mppi_get_stats",
+           "mppi_shift", "mppi_noise", "mppi_feynman_kac", "mppi_closed_loop", "mppi_plant_step", "mppi_get_stats",
            "mppi_last_launch_count", "mppi_profile_enable", "mppi_profile_read", "mppi_last_error", "mppi_status_string", "mppi_abi_version"]
 
 _lib = None
@@ -138,6 +138,8 @@ def lib():
     L.mppi_apply.restype = st
     L.mppi_shift.argtypes = [vp, vp, fp]
     L.mppi_shift.restype = st
+    L.mppi_closed_loop.argtypes = [vp, vp, vp, C.c_uint64, C.c_uint64, C.c_int32, fp, C.c_int32, vp, vp, vp]
+    L.mppi_closed_loop.restype = st
     L.mppi_feynman_kac.argtypes = [vp, fp, C.c_uint64, C.c_uint64, dp]
     L.mppi_feynman_kac.restype = st
     L.mppi_noise.argtypes = [vp, C.c_uint64, C.c_uint64, vp]

@@ -59,7 +59,7 @@ struct GraphState {
 struct DeviceStats {
     long long min_key;
     float eta;
-    float pad;
+    int plant_crashed;   // crash flag of the device-resident plant (mppi_closed_loop)
 };
 
 struct Ctx {
@@ -102,6 +102,7 @@ struct Ctx {
     // CUDA-graph replay of mppi_optimize (world == 1): [0] generated noise, [1] supplied noise
     bool use_graph = true;
     bool collect = false;                 // launchers append to `pending` instead of launching
+    bool x0_on_device = false;            // launch_rollout's x0 is a device pointer (closed loop)
     std::vector<KLaunch> pending;
     GraphState graphs[2];
 };
@@ -128,6 +129,8 @@ cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* 
 cudaError_t launch_shift(Ctx& c, float* U, const float* u_init);
 int wsum_blocks_per_sm(int m);  // resident wsum CTAs per SM (occupancy API)
 cudaError_t launch_fk_reduce(Ctx& c, double* part, int nblk);   // Feynman-Kac partial sums
+cudaError_t launch_advance(Ctx& c, float* x, float* U, const float* u_init, float* x_log,
+                           float* u_log, float* q_log);             // closed-loop plant step + shift
 
 // host plant step (mppi_runtime.cu uses it for mppi_plant_step)
 float host_plant_step(const Ctx& c, float* x, const float* u, int32_t* crashed);

@@ -162,6 +162,7 @@ struct RolloutArgs {
     float sd[4];            // diagonal path: s_i = sL[i][i]
     float ad[4];            // diagonal path: a_i = (1 - 1/nu)/2 R_ii s_i^2
     float x0[16];
+    const float* x0_dev;    // device-resident x0 (closed loop) or nullptr: use x0[]
     PP P;
     float4 obs_k[kMaxStaticPairs];  // negated obstacle pairs again, in the parameter constant bank
 };
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
     long long key = LLONG_MAX;
     if (k < a.K_loc) {
         Plant st;
-        st.load(a.x0, 0);
+        st.load(a.x0_dev ? a.x0_dev : a.x0, 0);
         // compile-time pair count: read the forest from the kernel-parameter constant bank
         // (uniform-register operands, no per-thread registers); else shared memory
         const ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(kRolloutThreads, 4)
     long long key = LLONG_MAX;
     if (k < a.K_loc) {
         QuadrotorX2 st;
-        st.load(a.x0);
+        st.load(a.x0_dev ? a.x0_dev : a.x0);
         const ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
         const size_t row = (size_t)a.K_loc * M;
         V2 S = vb(0.0f);
@@ -532,6 +533,100 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeArgs a) {
     }
 }
 
+// ------------------------------------------------------------------------------ closed-loop advance
+// Alg. 1 after the update: send u_0 to the (simulated, noise-free) plant,
+// x <- x + F(x, u_0) dt with the plant's accurate path, then shift U (u_i = u_{i+1}, u_{T-1} =
+// u_init).  One CTA; the plant step runs on thread 0 from the shared-memory copy of U.
+template <class PP>
+struct AdvanceArgs {
+    float* x;              // [n] device state, in/out
+    float* U;              // [T][M]
+    int* crashed;          // device flag (quadrotor)
+    float* x_log;          // [n] row for x' or nullptr
+    float* u_log;          // [M] row for u_0 or nullptr
+    float* q_log;          // q(x') or nullptr
+    const float4* obs;
+    int n_obs_pairs;
+    int T, n;
+    float dt;
+    float4 u_init;
+    PP P;
+};
+
+template <class Plant>
+__global__ void __launch_bounds__(1024) advance_kernel(const __grid_constant__ AdvanceArgs<typename Plant::Params> a) {
+    constexpr int M = Plant::M;
+    extern __shared__ float sUa[];
+    const int TM = a.T * M;
+    for (int o = threadIdx.x; o < TM; o += blockDim.x) sUa[o] = a.U[o];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Plant st;
+        float xin[16] = {0};
+        for (int i = 0; i < a.n; ++i) xin[i] = a.x[i];
+        st.load(xin, *a.crashed);
+        const ObstacleView ob{a.obs, a.n_obs_pairs};
+        float u0[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) u0[i] = sUa[i];
+        float xd[Plant::N];
+        st.template state_cost<-1>(true, a.P, ob);
+        st.deriv_accurate(u0, a.P, xd);
+        st.update(xd, a.dt);
+        const float q = st.template state_cost<-1>(false, a.P, ob);
+        float xo[16];
+        st.store(xo);
+        for (int i = 0; i < a.n; ++i) {
+            a.x[i] = xo[i];
+            if (a.x_log) a.x_log[i] = xo[i];
+        }
+        if (a.u_log)
+            for (int i = 0; i < M; ++i) a.u_log[i] = u0[i];
+        if (a.q_log) *a.q_log = q;
+        *a.crashed = st.crashed;
+    }
+    const float* ui = reinterpret_cast<const float*>(&a.u_init);
+    for (int o = threadIdx.x; o < TM; o += blockDim.x) a.U[o] = o < TM - M ? sUa[o + M] : ui[o - (TM - M)];
+}
+
+template <class Plant>
+static cudaError_t launch_advance_t(Ctx& c, const typename Plant::Params& P, float* x, float* U,
+                                    const float* u_init, float* x_log, float* u_log, float* q_log) {
+    AdvanceArgs<typename Plant::Params> a;
+    a.x = x;
+    a.U = U;
+    a.crashed = &c.d_stats->plant_crashed;
+    a.x_log = x_log;
+    a.u_log = u_log;
+    a.q_log = q_log;
+    a.obs = c.d_obs;
+    a.n_obs_pairs = c.n_obs_pairs;
+    a.T = c.T;
+    a.n = c.n;
+    a.dt = c.dt;
+    float* up = reinterpret_cast<float*>(&a.u_init);
+    for (int i = 0; i < 4; ++i) up[i] = i < c.m ? u_init[i] : 0.0f;
+    a.P = P;
+    const size_t smem = (size_t)c.T * c.m * sizeof(float);
+    auto kern = advance_kernel<Plant>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int threads = c.T * c.m >= 1024 ? 1024 : ((c.T * c.m + 31) / 32) * 32;
+    return emit(c, (const void*)kern, dim3(1), dim3(threads), smem, &a, sizeof(a), MPPI_KERNEL_SHIFT);
+}
+
+cudaError_t launch_advance(Ctx& c, float* x, float* U, const float* u_init, float* x_log, float* u_log,
+                           float* q_log) {
+    switch (c.plant) {
+        case MPPI_PLANT_CARTPOLE: return launch_advance_t<Cartpole>(c, c.params.cartpole, x, U, u_init, x_log, u_log, q_log);
+        case MPPI_PLANT_RACECAR: return launch_advance_t<Racecar>(c, c.params.racecar, x, U, u_init, x_log, u_log, q_log);
+        case MPPI_PLANT_QUADROTOR: return launch_advance_t<Quadrotor>(c, c.params.quadrotor, x, U, u_init, x_log, u_log, q_log);
+        default: return cudaErrorNotSupported;
+    }
+}
+
 // ------------------------------------------------------------------------------ Feynman-Kac reduction
 // partial sums of w_k = exp(-(S_k - S_min)/lambda) and w_k^2 per CTA, fp64, fixed order
 struct FkArgs {
@@ -701,7 +796,9 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
         a.sd[i] = i < c.m ? c.sL[i * c.m + i] : 0.0f;
         a.ad[i] = i < c.m ? c.ad[i] : 0.0f;
     }
-    for (int i = 0; i < c.n && i < 16; ++i) a.x0[i] = x0[i];
+    a.x0_dev = nullptr;
+    if (c.x0_on_device) a.x0_dev = x0;
+    else for (int i = 0; i < c.n && i < 16; ++i) a.x0[i] = x0[i];
     a.P = P;
     for (int i = 0; i < kMaxStaticPairs; ++i)
         a.obs_k[i] = i < c.n_obs_pairs ? c.obs_host[i] : make_float4(-1e15f, -1e15f, -1e15f, -1e15f);
@@ -764,6 +861,7 @@ cudaError_t launch_rollout(Ctx& c, const float* x0, const float* U, const float*
             return launch_rollout_p<Quadrotor>(c, c.params.quadrotor, x0, U, eps, costs_out);
         case MPPI_PLANT_LINEAR: {
             float xp[16] = {0};
+            if (c.x0_on_device) return cudaErrorNotSupported;   // linear test plant: host x0 only
             for (int i = 0; i < c.n; ++i) xp[i] = x0[i];
             if (c.m == 1) return launch_rollout_p<Linear<1>>(c, c.params.linear, xp, U, eps, costs_out);
             if (c.m == 2) return launch_rollout_p<Linear<2>>(c, c.params.linear, xp, U, eps, costs_out);

@@ -384,7 +384,7 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
     DeviceStats st0;
     st0.min_key = LLONG_MAX;
     st0.eta = 0.0f;
-    st0.pad = 0.0f;
+    st0.plant_crashed = 0;
     if ((e = cudaMemcpy(c.d_key_init, &kinit, sizeof(kinit), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMemcpy(c.d_stats, &st0, sizeof(st0), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (c.n_obs_pairs > 0 &&
@@ -622,6 +622,57 @@ mppi_status_t mppi_get_stats(mppi_ctx* ctx, mppi_stats_t* out) {
 }
 
 int32_t mppi_last_launch_count(const mppi_ctx* ctx) { return ctx ? ctx->c.last_launches : 0; }
+
+mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed, uint64_t step0,
+                               int32_t n_steps, const float* u_init, int32_t reset_crash,
+                               float* x_log, float* u_log, float* q_log) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (c.world != 1) return fail(MPPI_ERR_UNSUPPORTED, "mppi_closed_loop needs world == 1");
+    if (c.plant == MPPI_PLANT_LINEAR) return fail(MPPI_ERR_UNSUPPORTED, "mppi_closed_loop: linear test plant");
+    if (!x || !U || !u_init || n_steps < 1) return fail(MPPI_ERR_INVALID_ARG, "x, U, u_init non-NULL, n_steps >= 1");
+    if (!all_finite(u_init, c.m)) return fail(MPPI_ERR_INVALID_ARG, "u_init must be finite");
+    if (mppi_status_t s = sticky_check(c)) return s;
+    if (reset_crash)
+        MPPI_CUDA(cudaMemsetAsync(&c.d_stats->plant_crashed, 0, sizeof(int), c.stream), "crash reset");
+    // collect n_steps x [noise, rollout (x0 from device), wsum, finalize, advance] into one graph
+    c.last_launches = 0;
+    c.pending.clear();
+    c.collect = true;
+    c.x0_on_device = true;
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < n_steps && e == cudaSuccess; ++i) {
+        e = launch_noise(c, seed, step0 + (uint64_t)i, c.d_eps, true);
+        if (e == cudaSuccess) e = launch_rollout(c, x, U, c.d_eps, nullptr);
+        if (e == cudaSuccess) e = launch_wsum(c, c.d_eps, &c.d_stats->min_key);
+        if (e == cudaSuccess) e = launch_finalize(c, nullptr, nullptr, U);
+        if (e == cudaSuccess)
+            e = launch_advance(c, x, U, u_init, x_log ? x_log + (size_t)(i + 1) * c.n : nullptr,
+                               u_log ? u_log + (size_t)i * c.m : nullptr, q_log ? q_log + i : nullptr);
+    }
+    c.collect = false;
+    c.x0_on_device = false;
+    if (e != cudaSuccess) return cuda_fail(e, "collecting the closed loop");
+    if (x_log) MPPI_CUDA(cudaMemcpyAsync(x_log, x, (size_t)c.n * sizeof(float), cudaMemcpyDeviceToDevice, c.stream), "x_log[0]");
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    MPPI_CUDA(cudaGraphCreate(&g, 0), "cudaGraphCreate");
+    cudaGraphNode_t prev = nullptr;
+    for (KLaunch& L : c.pending) {
+        cudaKernelNodeParams p = node_params(L);
+        cudaGraphNode_t node;
+        cudaError_t ee = cudaGraphAddKernelNode(&node, g, prev ? &prev : nullptr, prev ? 1 : 0, &p);
+        if (ee != cudaSuccess) { cudaGraphDestroy(g); return cuda_fail(ee, "closed-loop graph"); }
+        prev = node;
+    }
+    e = cudaGraphInstantiate(&exec, g, 0);
+    if (e == cudaSuccess) e = cudaGraphLaunch(exec, c.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+    if (exec) cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "closed-loop graph launch");
+    return MPPI_OK;
+}
 
 mppi_status_t mppi_feynman_kac(mppi_ctx* ctx, const float* x0, uint64_t seed, uint64_t step, double* out) {
     if (mppi_status_t s = check_ctx(ctx)) return s;

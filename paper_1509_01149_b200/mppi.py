@@ -167,6 +167,24 @@ class MPPI:
         A.check(self.lib.mppi_noise(self.ctx, seed, step, _fptr(out)))
         return out
 
+    def closed_loop(self, x, U, n_steps, seed=0, step0=0, u_init=None, reset_crash=True, log=True):
+        """mppi_closed_loop: n_steps of Alg. 1 on the device (x: CUDA [n], U: CUDA [T][m], in/out).
+        Returns (x_log [n_steps+1][n], u_log [n_steps][m], q_log [n_steps]) CUDA tensors or None."""
+        _check_dev(x, (self.n,), torch.float32, "x")
+        _check_dev(U, (self.T, self.m), torch.float32, "U")
+        ui = _host_f32(np.zeros(self.m) if u_init is None else u_init, self.m, "u_init")
+        xl = ul = ql = None
+        if log:
+            xl = torch.empty((n_steps + 1, self.n), dtype=torch.float32, device=x.device)
+            ul = torch.empty((n_steps, self.m), dtype=torch.float32, device=x.device)
+            ql = torch.empty((n_steps,), dtype=torch.float32, device=x.device)
+        self._sync_stream()
+        A.check(self.lib.mppi_closed_loop(
+            self.ctx, _fptr(x), _fptr(U), seed, step0, int(n_steps), ui.ctypes.data_as(C.POINTER(C.c_float)),
+            1 if reset_crash else 0, _fptr(xl) if log else None, _fptr(ul) if log else None,
+            _fptr(ql) if log else None))
+        return (xl, ul, ql) if log else None
+
     def feynman_kac(self, x0, seed=0, step=0):
         """mppi_feynman_kac (PAPER.md:71-79): returns (log_psi, se_log_psi, s_min)."""
         x = self._x0(x0)
