@@ -454,7 +454,7 @@ struct NeumaierSum {
 template <class M>
 double rollout_one(const oracle_problem* pb, const double* Lsc /* sqrt(nu) L */,
                    const double* x0, const double* U, const float* eps, int64_t K, int64_t k,
-                   int* crashed_out) {
+                   int* crashed_out, double* qstep = nullptr /* [T]: q~ of each step, or null */) {
     typedef typename M::S S;
     const int n = pb->n, m = pb->m, T = pb->T;
     S x[16];
@@ -485,6 +485,7 @@ double rollout_one(const oracle_problem* pb, const double* Lsc /* sqrt(nu) L */,
         // q~ = q + (1-1/nu)/2 du'R du + u'R du + 1/2 u'R u
         S qt = q + c1 * duRdu + uRdu + (S)0.5 * uRu;
         Stilde += qt;                                 // S~ += q~  (no dt: A2)
+        if (qstep) qstep[t] = (double)qt;
     }
     // phi(x_T) = 0 for all three tasks
     if (crashed_out) *crashed_out = crashed;
@@ -657,6 +658,72 @@ int oracle_update(const oracle_problem* pb, const double* costs, const float* ep
     if (smin_out) *smin_out = smin;
     if (eta_out) *eta_out = etav;
     if (weights_out) for (int64_t k = 0; k < K; ++k) weights_out[k] = w[k];
+    return 0;
+}
+
+// Per-step augmented costs q~_{t,k} (fp64), out[k*T + t].  For the cost-to-go weighting.
+int oracle_rollout_stepcosts(const oracle_problem* pb, const double* x0, const double* U,
+                             const float* eps, int64_t K, int32_t nthreads, double* out) {
+    if (!problem_ok(pb) || K < 0) return 1;
+    double L[16], Lsc[16];
+    if (!cholesky(pb->Sigma, pb->m, L)) return 2;
+    const double s = std::sqrt(pb->nu);
+    for (int i = 0; i < pb->m * pb->m; ++i) Lsc[i] = s * L[i];
+#ifdef _OPENMP
+    int nt = nthreads > 0 ? nthreads : omp_get_max_threads();
+#pragma omp parallel for num_threads(nt) schedule(static)
+#endif
+    for (int64_t k = 0; k < K; ++k) {
+        int c = 0;
+        rollout_one<MathD>(pb, Lsc, x0, U, eps, K, k, &c, out + k * pb->T);
+    }
+    return 0;
+}
+
+// PAPER.md:320 / Alg. 1 :367 literally: per timestep i the weights use the cost-to-go
+//   S~(tau_{i,k}) = sum_{j >= i} q~_{j,k}      ("from time t_i onward"; phi = 0)
+//   w_{i,k} = exp(-(S~_{i,k} - min_k S~_{i,k}) / lambda),  eta_i = sum_k w_{i,k},
+//   U_i += sum_k w_{i,k} du_{i,k} / eta_i.
+// stepcosts[k*T + t] = q~_{t,k}; a non-finite cost-to-go is charged the penalty.
+// smin_out (optional, T) and eta_out (optional, T).  Sums in increasing k, Neumaier.
+int oracle_update_ctg(const oracle_problem* pb, const double* stepcosts, const float* eps,
+                      int64_t K, double* U, double* smin_out, double* eta_out) {
+    if (!problem_ok(pb) || K < 1) return 1;
+    const int m = pb->m, T = pb->T;
+    double L[16];
+    if (!cholesky(pb->Sigma, m, L)) return 2;
+    const double s = std::sqrt(pb->nu);
+    std::vector<double> ctg((size_t)K * T);
+    for (int64_t k = 0; k < K; ++k) {
+        NeumaierSum acc;
+        for (int t = T - 1; t >= 0; --t) {
+            acc.add(stepcosts[k * T + t]);
+            double v = acc.value();
+            ctg[(size_t)k * T + t] = std::isfinite(v) ? v : pb->penalty;
+        }
+    }
+    for (int t = 0; t < T; ++t) {
+        double smin = ctg[t];
+        for (int64_t k = 1; k < K; ++k) smin = std::min(smin, ctg[(size_t)k * T + t]);
+        std::vector<double> w(K);
+        NeumaierSum eta;
+        for (int64_t k = 0; k < K; ++k) {
+            w[k] = std::exp(-(ctg[(size_t)k * T + t] - smin) / pb->lambda);
+            eta.add(w[k]);
+        }
+        for (int i = 0; i < m; ++i) {
+            NeumaierSum num;
+            for (int64_t k = 0; k < K; ++k) {
+                const float* e = eps + ((int64_t)t * K + k) * m;
+                double du = 0.0;
+                for (int j = 0; j <= i; ++j) du += s * L[i * m + j] * (double)e[j];
+                num.add(w[k] * du);
+            }
+            U[t * m + i] += num.value() / eta.value();
+        }
+        if (smin_out) smin_out[t] = smin;
+        if (eta_out) eta_out[t] = eta.value();
+    }
     return 0;
 }
 

@@ -95,6 +95,8 @@ def lib():
         L.oracle_update.argtypes = [pp, dp, fp, C.c_int64, dp, lp, dp, dp, dp]
         L.oracle_optimize.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int32, dp, lp, dp]
         L.oracle_shift.argtypes = [dp, C.c_int32, C.c_int32, dp]
+        L.oracle_rollout_stepcosts.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int32, dp]
+        L.oracle_update_ctg.argtypes = [pp, dp, fp, C.c_int64, dp, dp, dp]
         L.oracle_trajectory.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int64, dp]
         _LIB = L
     return _LIB
@@ -239,6 +241,29 @@ def optimize(pb: Problem, x0, U, eps, nthreads=0):
     costs = rollout_costs(pb, x0, U, eps, nthreads=nthreads)
     U2, kstar, smin, eta, w = update(pb, costs, eps, U)
     return dict(U=U2, costs=costs, kstar=kstar, smin=smin, eta=eta, weights=w)
+
+
+def rollout_stepcosts(pb: Problem, x0, U, eps, nthreads=0):
+    """q~_{t,k} of every step, shape [K][T] (fp64)."""
+    x0 = np.ascontiguousarray(np.asarray(x0, np.float64))
+    U = np.ascontiguousarray(np.asarray(U, np.float64).reshape(pb.T, pb.m))
+    eps = np.ascontiguousarray(np.asarray(eps, np.float32))
+    K = eps.shape[1]
+    out = np.zeros((K, pb.T))
+    assert lib().oracle_rollout_stepcosts(pb.ptr(), _dp(x0), _dp(U), _fp(eps), K, nthreads, _dp(out)) == 0
+    return out
+
+
+def update_ctg(pb: Problem, stepcosts, eps, U):
+    """PAPER.md:320/:367 with per-timestep cost-to-go weights: returns (U', smin[T], eta[T])."""
+    sc = np.ascontiguousarray(np.asarray(stepcosts, np.float64))
+    eps = np.ascontiguousarray(np.asarray(eps, np.float32))
+    U2 = np.array(U, np.float64).reshape(pb.T, pb.m).copy()
+    K = sc.shape[0]
+    smin = np.zeros(pb.T)
+    eta = np.zeros(pb.T)
+    assert lib().oracle_update_ctg(pb.ptr(), _dp(sc), _fp(eps), K, _dp(U2), _dp(smin), _dp(eta)) == 0
+    return U2, smin, eta
 
 
 def shift(U, u_init):
