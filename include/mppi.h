@@ -297,6 +297,25 @@ mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, floa
  * order j = 0..i, U[t][i] = fl(U[t][i] + fl(d_i / eta)). */
 mppi_status_t mppi_apply(mppi_ctx* ctx, float* U, const float* buf);
 
+/* ---------------------------------------------------------------- cost-to-go weights (NEXT-1) */
+
+typedef enum {
+    MPPI_WEIGHTS_TRAJECTORY = 0,  /* w_k from the whole-horizon S~_k for every u_t (default) */
+    MPPI_WEIGHTS_COST_TO_GO = 1   /* PAPER.md:320-322 / Alg. 1 :367 literally: u_t weighted by
+                                     w_{t,k} = exp(-(S~_{t,k} - min_k S~_{t,k})/lambda) with the cost-to-go
+                                     S~_{t,k} = sum_{j >= t} q~_{j,k}; eta_t per timestep.  u_0 equals
+                                     the trajectory weighting's (S~_{0,k} = S~_k) up to rounding. */
+} mppi_weighting_t;
+
+/* mppi_set_weighting — selects the estimator of the update (synchronises the stream).  The
+ * cost-to-go mode allocates a [T][K_loc] fp32 buffer of per-step costs on first use, adds 8 B
+ * of HBM traffic per sample-step and a per-(t,k) exp; world == 1 only (else UNSUPPORTED). */
+mppi_status_t mppi_set_weighting(mppi_ctx* ctx, mppi_weighting_t mode);
+
+/* mppi_cost_to_go — copies S~_{t,k} of the last cost-to-go step into `out` (DEVICE float
+ * [T][K_loc]).  Asynchronous.  INVALID_ARG unless the cost-to-go weighting is enabled. */
+mppi_status_t mppi_cost_to_go(mppi_ctx* ctx, float* out);
+
 /* ---------------------------------------------------------------- on-device MPC loop (NEXT-2) */
 
 /* mppi_closed_loop — Algorithm 1's while-loop for n_steps receding-horizon

@@ -663,7 +663,7 @@ int oracle_update(const oracle_problem* pb, const double* costs, const float* ep
 
 // Per-step augmented costs q~_{t,k} (fp64), out[k*T + t].  For the cost-to-go weighting.
 int oracle_rollout_stepcosts(const oracle_problem* pb, const double* x0, const double* U,
-                             const float* eps, int64_t K, int32_t nthreads, double* out) {
+                             const float* eps, int64_t K, int32_t nthreads, double* out, int32_t mode) {
     if (!problem_ok(pb) || K < 0) return 1;
     double L[16], Lsc[16];
     if (!cholesky(pb->Sigma, pb->m, L)) return 2;
@@ -674,8 +674,10 @@ int oracle_rollout_stepcosts(const oracle_problem* pb, const double* x0, const d
 #pragma omp parallel for num_threads(nt) schedule(static)
 #endif
     for (int64_t k = 0; k < K; ++k) {
-        int c = 0;
-        rollout_one<MathD>(pb, Lsc, x0, U, eps, K, k, &c, out + k * pb->T);
+        int c = 0;   // mode as oracle_rollout_costs: 0 fp64, 1 / 2 the fp32 conditioning twins
+        if (mode == 1) rollout_one<MathF>(pb, Lsc, x0, U, eps, K, k, &c, out + k * pb->T);
+        else if (mode == 2) rollout_one<MathFviaD>(pb, Lsc, x0, U, eps, K, k, &c, out + k * pb->T);
+        else rollout_one<MathD>(pb, Lsc, x0, U, eps, K, k, &c, out + k * pb->T);
     }
     return 0;
 }

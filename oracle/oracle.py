@@ -95,7 +95,7 @@ def lib():
         L.oracle_update.argtypes = [pp, dp, fp, C.c_int64, dp, lp, dp, dp, dp]
         L.oracle_optimize.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int32, dp, lp, dp]
         L.oracle_shift.argtypes = [dp, C.c_int32, C.c_int32, dp]
-        L.oracle_rollout_stepcosts.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int32, dp]
+        L.oracle_rollout_stepcosts.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int32, dp, C.c_int32]
         L.oracle_update_ctg.argtypes = [pp, dp, fp, C.c_int64, dp, dp, dp]
         L.oracle_trajectory.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int64, dp]
         _LIB = L
@@ -243,15 +243,33 @@ def optimize(pb: Problem, x0, U, eps, nthreads=0):
     return dict(U=U2, costs=costs, kstar=kstar, smin=smin, eta=eta, weights=w)
 
 
-def rollout_stepcosts(pb: Problem, x0, U, eps, nthreads=0):
-    """q~_{t,k} of every step, shape [K][T] (fp64)."""
+def rollout_stepcosts(pb: Problem, x0, U, eps, nthreads=0, mode="fp64"):
+    """q~_{t,k} of every step, shape [K][T] (fp64; or an fp32 conditioning twin, see MODES)."""
     x0 = np.ascontiguousarray(np.asarray(x0, np.float64))
     U = np.ascontiguousarray(np.asarray(U, np.float64).reshape(pb.T, pb.m))
     eps = np.ascontiguousarray(np.asarray(eps, np.float32))
     K = eps.shape[1]
     out = np.zeros((K, pb.T))
-    assert lib().oracle_rollout_stepcosts(pb.ptr(), _dp(x0), _dp(U), _fp(eps), K, nthreads, _dp(out)) == 0
+    assert lib().oracle_rollout_stepcosts(pb.ptr(), _dp(x0), _dp(U), _fp(eps), K, nthreads, _dp(out),
+                                          MODES[mode]) == 0
     return out
+
+
+def cost_to_go(stepcosts):
+    """S~_{t,k} = sum_{j >= t} q~_{j,k}, shape [T][K] from [K][T] step costs."""
+    return np.cumsum(np.asarray(stepcosts)[:, ::-1], axis=1)[:, ::-1].T
+
+
+def well_conditioned_ctg(pb: Problem, x0, U, eps, rel=1e-5, nthreads=0):
+    """SURVEY A19 applied to the cost-to-go: sample k is well-conditioned iff at every t both fp32
+    twins' S~_{t,k} are within rel * max(|S~_{0,k}|, 1) of fp64.  Returns (mask[K], ctg fp64 [T][K])."""
+    ref = cost_to_go(rollout_stepcosts(pb, x0, U, eps, nthreads))
+    scale = np.maximum(np.abs(ref[0]), 1.0)
+    ok = np.ones(ref.shape[1], bool)
+    for mode in ("twin_f32", "twin_f32_via_f64"):
+        tw = cost_to_go(rollout_stepcosts(pb, x0, U, eps, nthreads, mode))
+        ok &= np.all(np.abs(tw - ref) <= rel * scale, axis=0)
+    return ok, ref
 
 
 def update_ctg(pb: Problem, stepcosts, eps, U):

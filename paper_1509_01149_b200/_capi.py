@@ -14,6 +14,7 @@ MPPI_OK, MPPI_ERR_INVALID_ARG, MPPI_ERR_NOT_SPD, MPPI_ERR_OOM, MPPI_ERR_CUDA, MP
 MPPI_PLANT_CARTPOLE, MPPI_PLANT_RACECAR, MPPI_PLANT_QUADROTOR, MPPI_PLANT_LINEAR = 1, 2, 3, 4
 MPPI_MAX_OBSTACLES = 4096
 MPPI_OPTION_CUDA_GRAPH, MPPI_OPTION_PACKED_SAMPLES = 1, 2
+MPPI_WEIGHTS_TRAJECTORY, MPPI_WEIGHTS_COST_TO_GO = 0, 1
 
 
 class cartpole_dynamics_t(C.Structure):
@@ -94,7 +95,8 @@ KERNEL_NAMES = ["noise", "rollout", "wsum", "finalize", "shift"]
 
 EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize", "mppi_use_graph", "mppi_set_option",
            "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_apply",
-           "mppi_shift", "mppi_noise", "mppi_feynman_kac", "mppi_closed_loop", "mppi_plant_step", "mppi_get_stats",
+           "mppi_shift", "mppi_noise", "mppi_feynman_kac", "mppi_closed_loop", "mppi_set_weighting",
+           "mppi_cost_to_go", "mppi_plant_step", "mppi_get_stats",
            "mppi_last_launch_count", "mppi_profile_enable", "mppi_profile_read", "mppi_last_error", "mppi_status_string", "mppi_abi_version"]
 
 _lib = None
@@ -138,6 +140,10 @@ def lib():
     L.mppi_apply.restype = st
     L.mppi_shift.argtypes = [vp, vp, fp]
     L.mppi_shift.restype = st
+    L.mppi_set_weighting.argtypes = [vp, C.c_int]
+    L.mppi_set_weighting.restype = st
+    L.mppi_cost_to_go.argtypes = [vp, vp]
+    L.mppi_cost_to_go.restype = st
     L.mppi_closed_loop.argtypes = [vp, vp, vp, C.c_uint64, C.c_uint64, C.c_int32, fp, C.c_int32, vp, vp, vp]
     L.mppi_closed_loop.restype = st
     L.mppi_feynman_kac.argtypes = [vp, fp, C.c_uint64, C.c_uint64, dp]

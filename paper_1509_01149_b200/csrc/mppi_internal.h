@@ -87,6 +87,12 @@ struct Ctx {
     DeviceStats* d_stats = nullptr;
     float* d_U = nullptr;           // [T][m] for mppi_optimize_host / mppi_feynman_kac
     double* d_fk = nullptr;         // Feynman-Kac partial sums (lazy)
+    // NEXT-1 per-timestep cost-to-go weighting (lazy workspace)
+    bool ctg = false;
+    float* d_ctg = nullptr;         // [T][K_loc] q~ then S~_{t,k}
+    float* d_ctg_partmin = nullptr; // [T][ceil(K_loc/256)]
+    float* d_ctg_smin = nullptr;    // [T]
+    float* d_ctg_eta = nullptr;     // [n_chunks][T]
     float* h_U_pinned = nullptr;    // pinned staging for mppi_optimize_host
     int n_chunks = 1;
     int64_t cols_per_chunk = 0;     // float4 columns of a noise row per chunk
@@ -129,6 +135,9 @@ cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* 
 cudaError_t launch_shift(Ctx& c, float* U, const float* u_init);
 int wsum_blocks_per_sm(int m);  // resident wsum CTAs per SM (occupancy API)
 cudaError_t launch_fk_reduce(Ctx& c, double* part, int nblk);   // Feynman-Kac partial sums
+cudaError_t launch_ctg(Ctx& c);                                  // cost-to-go + per-t minima
+cudaError_t launch_wsum_ctg(Ctx& c, const float* eps);
+cudaError_t launch_finalize_ctg(Ctx& c, float* U);
 cudaError_t launch_advance(Ctx& c, float* x, float* U, const float* u_init, float* x_log,
                            float* u_log, float* q_log);             // closed-loop plant step + shift
 

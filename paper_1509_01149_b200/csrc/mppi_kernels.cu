@@ -163,6 +163,7 @@ struct RolloutArgs {
     float ad[4];            // diagonal path: a_i = (1 - 1/nu)/2 R_ii s_i^2
     float x0[16];
     const float* x0_dev;    // device-resident x0 (closed loop) or nullptr: use x0[]
+    float* qstep;           // [T][K_loc] per-step q~_{t,k} (cost-to-go weighting) or nullptr
     PP P;
     float4 obs_k[kMaxStaticPairs];  // negated obstacle pairs again, in the parameter constant bank
 };
@@ -217,7 +218,8 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
         const ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
         const size_t row = (size_t)a.K_loc * M;
         float S = 0.0f;
-        auto one_step = [&](const StepRec* rec, const float* e, bool first) {
+        float is_prev = 0.0f;                                          // IS term of step t-1
+        auto one_step = [&](const StepRec* rec, const float* e, bool first, int t) {
             const float4 u4 = rec->u;
             const float4 b4 = rec->b;
             const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
@@ -256,6 +258,10 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
             if (st.deriv_fast(v, a.P, xd)) st.deriv_accurate(v, a.P, xd);   // |angle| > 105615: rare
             st.update(xd, a.dt);
             S += q + is;                                               // S~ += q~
+            if (a.qstep) {                                             // q~_{t-1} = q(x_t) + IS_{t-1}
+                if (!first) a.qstep[(size_t)(t - 1) * a.K_loc + k] = q + is_prev;
+                is_prev = is;
+            }
         };
         // eps ring: two slots, the copy for step t+1 is issued before step t is computed
         const float* gp = a.eps + (size_t)k * M;
@@ -272,10 +278,12 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
             cp_async_wait<1>();                                        // step t has landed
             float e[M];
             load_shared_eps<M>(cur, e);
-            one_step(rec, e, t == 0);
+            one_step(rec, e, t == 0, t);
             cur = slot_sum - cur;
         }
-        S += st.template state_cost<NP>(false, a.P, ob);              // q(x_T), step T-1
+        const float qT = st.template state_cost<NP>(false, a.P, ob);  // q(x_T), step T-1
+        S += qT;
+        if (a.qstep) a.qstep[(size_t)(a.T - 1) * a.K_loc + k] = qT + is_prev;
         if (!isfinite(S)) S = a.penalty;
         a.costs[k] = S;
         if (a.costs_out) a.costs_out[k] = S;
@@ -335,6 +343,7 @@ __global__ void __launch_bounds__(kRolloutThreads, 4)
         const ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
         const size_t row = (size_t)a.K_loc * M;
         V2 S = vb(0.0f);
+        V2 is_prev = vb(0.0f);
         const float* gp = a.eps + (size_t)k * M;                       // 32 contiguous bytes
         const unsigned slot0 = (unsigned)__cvta_generic_to_shared(sRing + tid * 2 * M);
         const unsigned slot_sum = 2u * slot0 + blockDim.x * 2 * M * (unsigned)sizeof(float);
@@ -370,9 +379,15 @@ __global__ void __launch_bounds__(kRolloutThreads, 4)
             if (st.deriv_fast(v, a.P, xd)) st.deriv_accurate(v, a.P, xd);
             st.update(xd, a.dt);
             S = S + (q + is);                                              // S~ += q~
+            if (a.qstep) {
+                if (t > 0) *reinterpret_cast<float2*>(a.qstep + (size_t)(t - 1) * a.K_loc + k) = (q + is_prev).v;
+                is_prev = is;
+            }
             cur = slot_sum - cur;
         }
-        S = S + st.template state_cost<NP>(false, a.P, ob);               // q(x_T)
+        const V2 qT = st.template state_cost<NP>(false, a.P, ob);         // q(x_T)
+        S = S + qT;
+        if (a.qstep) *reinterpret_cast<float2*>(a.qstep + (size_t)(a.T - 1) * a.K_loc + k) = (qT + is_prev).v;
         float sa = S.v.x, sb = S.v.y;
         if (!isfinite(sa)) sa = a.penalty;
         if (!isfinite(sb)) sb = a.penalty;
@@ -531,6 +546,229 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeArgs a) {
             a.U[o] = __fadd_rn(a.U[o], __fdiv_rn(d, eta));   // U_t += sum w du / eta
         }
     }
+}
+
+// ------------------------------------------------------------------------------ NEXT-1: cost-to-go
+// S~(tau_{t,k}) = sum_{j >= t} q~_{j,k} ("from time t_i onward"), in place over the
+// [T][K_loc] per-step costs, reverse order per sample (coalesced rows); non-finite -> penalty.
+// Per CTA and t the minimum over its samples goes to partmin[t][blockIdx.x].
+struct CtgArgs {
+    float* ctg;          // [T][K_loc] q~ in, S~ out
+    float* partmin;      // [T][nblk]
+    int T, K_loc, nblk;
+    float penalty;
+};
+
+__global__ void __launch_bounds__(256) ctg_kernel(const CtgArgs a) {
+    extern __shared__ float wmin_t[];   // [8 warps][T]
+    const int k = blockIdx.x * 256 + threadIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float s = 0.0f;
+    for (int t = a.T - 1; t >= 0; --t) {
+        float v = INFINITY;
+        if (k < a.K_loc) {
+            float* p = a.ctg + (size_t)t * a.K_loc + k;
+            s += *p;
+            v = isfinite(s) ? s : a.penalty;
+            *p = v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) wmin_t[warp * a.T + t] = v;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < a.T; t += 256) {
+        float v = wmin_t[t];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) v = fminf(v, wmin_t[w * a.T + t]);
+        a.partmin[(size_t)t * a.nblk + blockIdx.x] = v;
+    }
+}
+
+// smin[t] = min over CTAs of partmin[t][.]  (one CTA per t; min is exact, order-free)
+struct CtgMinArgs {
+    const float* partmin;
+    int nblk;
+    float* smin;
+};
+
+__global__ void __launch_bounds__(256) ctg_min_kernel(const CtgMinArgs a) {
+    const int t = blockIdx.x;
+    float v = INFINITY;
+    for (int i = threadIdx.x; i < a.nblk; i += 256) v = fminf(v, a.partmin[(size_t)t * a.nblk + i]);
+    __shared__ float r[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = r[0];
+        for (int w = 1; w < 8; ++w) m = fminf(m, r[w]);
+        a.smin[t] = m;
+    }
+}
+
+// A[t][j] = sum_k w_{t,k} eps[t][k][j], eta_t = sum_k w_{t,k}, w_{t,k} = exp(-(S~_{t,k} - smin_t)/lambda)
+// (PAPER.md:320 with per-timestep weights).  Same tiling and fixed-order reduction as wsum_kernel.
+struct WsumCtgArgs {
+    const float* eps;
+    const float* ctg;     // [T][K_loc]
+    const float* smin;    // [T]
+    float* part;          // [n_chunks][T][M]
+    float* eta_part;      // [n_chunks][T]
+    int T, K_loc;
+    long long ncols, cols_per_chunk;
+    float lambda;
+};
+
+template <int M>
+__global__ void __launch_bounds__(kWsumThreads) wsum_ctg_kernel(const WsumCtgArgs a) {
+    constexpr int SPC = 4 / M;
+    constexpr int TT = kWsumTT;
+    const int chunk = blockIdx.x;
+    const int t0 = blockIdx.y * TT;
+    const int nt = min(TT, a.T - t0);
+    const long long c_begin = (long long)chunk * a.cols_per_chunk;
+    const long long c_end = min(a.ncols, c_begin + a.cols_per_chunk);
+    const float4* __restrict__ eps4 = reinterpret_cast<const float4*>(a.eps);
+    float acc[TT][4], eta[TT];
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt) {
+        eta[tt] = 0.0f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[tt][c] = 0.0f;
+    }
+    for (long long col = c_begin + threadIdx.x; col < c_end; col += kWsumThreads) {
+#pragma unroll
+        for (int tt = 0; tt < TT; ++tt) {
+            if (tt < nt) {
+                const int t = t0 + tt;
+                const float sm = a.smin[t];
+                const float* crow = a.ctg + (size_t)t * a.K_loc + col * SPC;
+                float w[SPC];
+#pragma unroll
+                for (int s = 0; s < SPC; ++s) {
+                    w[s] = expf(-__fdiv_rn(crow[s] - sm, a.lambda));
+                    eta[tt] += w[s];
+                }
+                const float4 v = __ldcs(eps4 + (size_t)t * a.ncols + col);
+                acc[tt][0] = fmaf(w[0 / M], v.x, acc[tt][0]);
+                acc[tt][1] = fmaf(w[1 / M], v.y, acc[tt][1]);
+                acc[tt][2] = fmaf(w[2 / M], v.z, acc[tt][2]);
+                acc[tt][3] = fmaf(w[3 / M], v.w, acc[tt][3]);
+            }
+        }
+    }
+    __shared__ float red[kWsumThreads / 32][TT * (M + 1)];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt) {
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            float f = 0.0f;
+#pragma unroll
+            for (int s = 0; s < SPC; ++s) f += acc[tt][s * M + j];
+            f = warp_sum(f);
+            if (lane == 0) red[warp][tt * M + j] = f;
+        }
+        const float e = warp_sum(eta[tt]);
+        if (lane == 0) red[warp][TT * M + tt] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x < TT * (M + 1)) {
+        float s = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kWsumThreads / 32; ++w) s += red[w][threadIdx.x];
+        if (threadIdx.x < TT * M) {
+            const int tt = threadIdx.x / M, j = threadIdx.x % M;
+            if (tt < nt) a.part[((size_t)chunk * a.T + t0 + tt) * M + j] = s;
+        } else {
+            const int tt = threadIdx.x - TT * M;
+            if (tt < nt) a.eta_part[(size_t)chunk * a.T + t0 + tt] = s;
+        }
+    }
+}
+
+// U_t += sqrt(nu) L A_t / eta_t (per-timestep normalisers), fixed order over chunks
+struct FinalizeCtgArgs {
+    const float* part;
+    const float* eta_part;
+    int n_chunks;
+    float* U;
+    DeviceStats* stats;
+    int T, M;
+    float sL[16];
+};
+
+__global__ void __launch_bounds__(1024) finalize_ctg_kernel(const FinalizeCtgArgs a) {
+    const int TM = a.T * a.M;
+    for (int o = threadIdx.x; o < TM; o += blockDim.x) {
+        const int t = o / a.M, i = o % a.M;
+        float eta = 0.0f;
+        for (int c = 0; c < a.n_chunks; ++c) eta += a.eta_part[(size_t)c * a.T + t];
+        float d = 0.0f;
+        for (int j = 0; j <= i; ++j) {
+            float A = 0.0f;
+            for (int c = 0; c < a.n_chunks; ++c) A += a.part[((size_t)c * a.T + t) * a.M + j];
+            d = __fadd_rn(d, __fmul_rn(a.sL[i * a.M + j], A));
+        }
+        a.U[o] = __fadd_rn(a.U[o], __fdiv_rn(d, eta));
+        if (o == 0 && a.stats) a.stats->eta = eta;
+    }
+}
+
+cudaError_t launch_ctg(Ctx& c) {
+    const int nblk = (int)((c.K_loc + 255) / 256);
+    CtgArgs a;
+    a.ctg = c.d_ctg;
+    a.partmin = c.d_ctg_partmin;
+    a.T = c.T;
+    a.K_loc = (int)c.K_loc;
+    a.nblk = nblk;
+    a.penalty = c.penalty;
+    const size_t smem = (size_t)8 * c.T * sizeof(float);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(ctg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = emit(c, (const void*)ctg_kernel, dim3(nblk), dim3(256), smem, &a, sizeof(a), MPPI_KERNEL_WSUM);
+    if (e != cudaSuccess) return e;
+    CtgMinArgs m{c.d_ctg_partmin, nblk, c.d_ctg_smin};
+    return emit(c, (const void*)ctg_min_kernel, dim3(c.T), dim3(256), 0, &m, sizeof(m), MPPI_KERNEL_WSUM);
+}
+
+cudaError_t launch_wsum_ctg(Ctx& c, const float* eps) {
+    WsumCtgArgs a;
+    a.eps = eps;
+    a.ctg = c.d_ctg;
+    a.smin = c.d_ctg_smin;
+    a.part = c.d_part;
+    a.eta_part = c.d_ctg_eta;
+    a.T = c.T;
+    a.K_loc = (int)c.K_loc;
+    a.ncols = c.K_loc * c.m / 4;
+    a.cols_per_chunk = c.cols_per_chunk;
+    a.lambda = c.lambda;
+    const dim3 grid((unsigned)c.n_chunks, (unsigned)((c.T + kWsumTT - 1) / kWsumTT));
+    const void* f = c.m == 1 ? (const void*)wsum_ctg_kernel<1> : c.m == 2 ? (const void*)wsum_ctg_kernel<2>
+                  : c.m == 4 ? (const void*)wsum_ctg_kernel<4> : nullptr;
+    if (!f) return cudaErrorInvalidValue;
+    return emit(c, f, grid, dim3(kWsumThreads), 0, &a, sizeof(a), MPPI_KERNEL_WSUM);
+}
+
+cudaError_t launch_finalize_ctg(Ctx& c, float* U) {
+    FinalizeCtgArgs a;
+    a.part = c.d_part;
+    a.eta_part = c.d_ctg_eta;
+    a.n_chunks = c.n_chunks;
+    a.U = U;
+    a.stats = c.d_stats;
+    a.T = c.T;
+    a.M = c.m;
+    for (int i = 0; i < 16; ++i) a.sL[i] = c.sL[i];
+    const int threads = c.T * c.m >= 1024 ? 1024 : ((c.T * c.m + 31) / 32) * 32;
+    return emit(c, (const void*)finalize_ctg_kernel, dim3(1), dim3(threads), 0, &a, sizeof(a),
+                MPPI_KERNEL_FINALIZE);
 }
 
 // ------------------------------------------------------------------------------ closed-loop advance
@@ -797,6 +1035,7 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
         a.ad[i] = i < c.m ? c.ad[i] : 0.0f;
     }
     a.x0_dev = nullptr;
+    a.qstep = c.ctg ? c.d_ctg : nullptr;
     if (c.x0_on_device) a.x0_dev = x0;
     else for (int i = 0; i < c.n && i < 16; ++i) a.x0[i] = x0[i];
     a.P = P;

@@ -207,6 +207,10 @@ void free_ctx(Ctx& c) {
     cudaFree(c.d_stats);
     cudaFree(c.d_U);
     cudaFree(c.d_fk);
+    cudaFree(c.d_ctg);
+    cudaFree(c.d_ctg_partmin);
+    cudaFree(c.d_ctg_smin);
+    cudaFree(c.d_ctg_eta);
     if (c.h_U_pinned) cudaFreeHost(c.h_U_pinned);
 }
 
@@ -427,6 +431,18 @@ mppi_status_t mppi_set_stream(mppi_ctx* ctx, void* cuda_stream) {
     return MPPI_OK;
 }
 
+// the update after the rollout: trajectory weights (K3 + K4) or per-timestep cost-to-go weights
+static cudaError_t launch_reduce_update(Ctx& c, const float* eps, float* U) {
+    cudaError_t e;
+    if (c.ctg) {
+        if ((e = launch_ctg(c)) != cudaSuccess) return e;
+        if ((e = launch_wsum_ctg(c, eps)) != cudaSuccess) return e;
+        return launch_finalize_ctg(c, U);
+    }
+    if ((e = launch_wsum(c, eps, &c.d_stats->min_key)) != cudaSuccess) return e;
+    return launch_finalize(c, nullptr, nullptr, U);
+}
+
 static cudaKernelNodeParams node_params(KLaunch& L) {
     cudaKernelNodeParams p = {};
     p.func = const_cast<void*>(L.func);
@@ -454,8 +470,7 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
     cudaError_t e = cudaSuccess;
     if (!noise) e = launch_noise(c, seed, step, c.d_eps, true);
     if (e == cudaSuccess) e = launch_rollout(c, x0, U, eps, nullptr);
-    if (e == cudaSuccess) e = launch_wsum(c, eps, &c.d_stats->min_key);
-    if (e == cudaSuccess) e = launch_finalize(c, nullptr, nullptr, U);
+    if (e == cudaSuccess) e = launch_reduce_update(c, eps, U);
     c.collect = false;
     if (e != cudaSuccess) return cuda_fail(e, "collecting the step's launches");
     GraphState& G = c.graphs[noise ? 1 : 0];
@@ -516,8 +531,38 @@ mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t s
     c.last_launches = 0;
     const float* eps = nullptr;
     if (mppi_status_t s = do_rollout(c, x0, U, seed, step, noise, nullptr, &eps)) return s;
-    MPPI_CUDA(launch_wsum(c, eps, &c.d_stats->min_key), "wsum_kernel launch");
-    MPPI_CUDA(launch_finalize(c, nullptr, nullptr, U), "finalize_kernel launch");
+    MPPI_CUDA(launch_reduce_update(c, eps, U), "reduction/update launch");
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_set_weighting(mppi_ctx* ctx, mppi_weighting_t mode) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (mode != MPPI_WEIGHTS_TRAJECTORY && mode != MPPI_WEIGHTS_COST_TO_GO)
+        return fail(MPPI_ERR_INVALID_ARG, "unknown weighting %d", (int)mode);
+    if (mode == MPPI_WEIGHTS_COST_TO_GO && !c.d_ctg) {
+        if (c.world != 1) return fail(MPPI_ERR_UNSUPPORTED, "cost-to-go weighting needs world == 1");
+        const int64_t nblk = (c.K_loc + 255) / 256;
+        mppi_status_t a;
+        if ((a = dalloc(c, &c.d_ctg, (size_t)c.T * c.K_loc, "cost-to-go")) ||
+            (a = dalloc(c, &c.d_ctg_partmin, (size_t)c.T * nblk, "cost-to-go minima")) ||
+            (a = dalloc(c, &c.d_ctg_smin, (size_t)c.T, "cost-to-go smin")) ||
+            (a = dalloc(c, &c.d_ctg_eta, (size_t)c.n_chunks * c.T, "cost-to-go eta")))
+            return a;
+    }
+    MPPI_CUDA(cudaStreamSynchronize(c.stream), "stream sync");
+    c.ctg = mode == MPPI_WEIGHTS_COST_TO_GO;
+    free_graphs(c);     // the step's kernel sequence changed
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_cost_to_go(mppi_ctx* ctx, float* out) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
+    if (!c.ctg) return fail(MPPI_ERR_INVALID_ARG, "cost-to-go weighting is not enabled");
+    MPPI_CUDA(cudaMemcpyAsync(out, c.d_ctg, (size_t)c.T * c.K_loc * sizeof(float), cudaMemcpyDeviceToDevice,
+                              c.stream), "cost-to-go copy");
     return MPPI_OK;
 }
 
@@ -644,8 +689,7 @@ mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed,
     for (int i = 0; i < n_steps && e == cudaSuccess; ++i) {
         e = launch_noise(c, seed, step0 + (uint64_t)i, c.d_eps, true);
         if (e == cudaSuccess) e = launch_rollout(c, x, U, c.d_eps, nullptr);
-        if (e == cudaSuccess) e = launch_wsum(c, c.d_eps, &c.d_stats->min_key);
-        if (e == cudaSuccess) e = launch_finalize(c, nullptr, nullptr, U);
+        if (e == cudaSuccess) e = launch_reduce_update(c, c.d_eps, U);
         if (e == cudaSuccess)
             e = launch_advance(c, x, U, u_init, x_log ? x_log + (size_t)(i + 1) * c.n : nullptr,
                                u_log ? u_log + (size_t)i * c.m : nullptr, q_log ? q_log + i : nullptr);

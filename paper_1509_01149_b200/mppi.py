@@ -167,6 +167,20 @@ class MPPI:
         A.check(self.lib.mppi_noise(self.ctx, seed, step, _fptr(out)))
         return out
 
+    def set_weighting(self, cost_to_go):
+        """mppi_set_weighting: per-timestep cost-to-go weights or trajectory."""
+        A.check(self.lib.mppi_set_weighting(
+            self.ctx, A.MPPI_WEIGHTS_COST_TO_GO if cost_to_go else A.MPPI_WEIGHTS_TRAJECTORY))
+
+    def cost_to_go(self, out=None):
+        """mppi_cost_to_go: S~_{t,k} of the last cost-to-go step, CUDA [T][K_loc]."""
+        if out is None:
+            out = torch.empty((self.T, self.K_loc), dtype=torch.float32, device=self.device)
+        _check_dev(out, (self.T, self.K_loc), torch.float32, "out")
+        self._sync_stream()
+        A.check(self.lib.mppi_cost_to_go(self.ctx, _fptr(out)))
+        return out
+
     def closed_loop(self, x, U, n_steps, seed=0, step0=0, u_init=None, reset_crash=True, log=True):
         """mppi_closed_loop: n_steps of Alg. 1 on the device (x: CUDA [n], U: CUDA [T][m], in/out).
         Returns (x_log [n_steps+1][n], u_log [n_steps][m], q_log [n_steps]) CUDA tensors or None."""
