@@ -220,6 +220,7 @@ extern "C" typedef struct {
     int32_t n_obstacles;
     const double* obstacles;  // n_obstacles*2 (x, y) cylinder centres (quadrotor)
     double penalty;           // cost of a non-finite rollout
+    const double* At;         // optional [T][m][m] sampling transforms A_t (NEXT-3); null: sqrt(nu) I
 } oracle_problem;
 
 namespace {
@@ -439,6 +440,56 @@ bool cholesky(const double* A, int m, double* L) {
     return true;
 }
 
+// Gauss-Jordan inverse of an m x m matrix (fp64, partial pivoting).  false if singular.
+bool invert(const double* A, int m, double* Ai) {
+    double a[16], b[16];
+    for (int i = 0; i < m * m; ++i) { a[i] = A[i]; b[i] = 0.0; }
+    for (int i = 0; i < m; ++i) b[i * m + i] = 1.0;
+    for (int c = 0; c < m; ++c) {
+        int p = c;
+        for (int r = c + 1; r < m; ++r)
+            if (std::fabs(a[r * m + c]) > std::fabs(a[p * m + c])) p = r;
+        if (a[p * m + c] == 0.0) return false;
+        for (int j = 0; j < m; ++j) { std::swap(a[c * m + j], a[p * m + j]); std::swap(b[c * m + j], b[p * m + j]); }
+        const double d = a[c * m + c];
+        for (int j = 0; j < m; ++j) { a[c * m + j] /= d; b[c * m + j] /= d; }
+        for (int r = 0; r < m; ++r) {
+            if (r == c) continue;
+            const double f = a[r * m + c];
+            for (int j = 0; j < m; ++j) { a[r * m + j] -= f * a[c * m + j]; b[r * m + j] -= f * b[c * m + j]; }
+        }
+    }
+    for (int i = 0; i < m * m; ++i) Ai[i] = b[i];
+    return true;
+}
+
+// Per-step sampling factor and importance-sampling matrix (NEXT-3, Theorem 1, PAPER.md:177-201,
+// :271-284 in control coordinates with Eq. 7: Sigma~ = R^{-1}, Lambda~_t = A_t R^{-1} A_t^T):
+//   du_t = F_t eps,  F_t = A_t L              (default A_t = sqrt(nu) I: F = sqrt(nu) L)
+//   Gamma~_t^{-1} = R - A_t^{-T} R A_t^{-1}    (default: (1 - 1/nu) R)
+bool step_matrices(const oracle_problem* pb, int t, const double* L, double* F, double* Gi) {
+    const int m = pb->m;
+    if (!pb->At) {
+        const double s = std::sqrt(pb->nu);
+        for (int i = 0; i < m * m; ++i) { F[i] = s * L[i]; Gi[i] = (1.0 - 1.0 / pb->nu) * pb->R[i]; }
+        return true;
+    }
+    const double* A = pb->At + (size_t)t * m * m;
+    double Ai[16];
+    if (!invert(A, m, Ai)) return false;
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) {
+            double f = 0.0;
+            for (int k = 0; k < m; ++k) f += A[i * m + k] * L[k * m + j];
+            F[i * m + j] = f;
+            double g = 0.0;                       // (A^{-T} R A^{-1})_{ij}
+            for (int k = 0; k < m; ++k)
+                for (int l = 0; l < m; ++l) g += Ai[k * m + i] * pb->R[k * m + l] * Ai[l * m + j];
+            Gi[i * m + j] = pb->R[i * m + j] - g;
+        }
+    return true;
+}
+
 // Neumaier-compensated running sum (for the k-ordered reductions of PAPER.md:320)
 struct NeumaierSum {
     double s = 0.0, c = 0.0;
@@ -452,38 +503,43 @@ struct NeumaierSum {
 
 // One rollout of sample k.  eps row layout [T][K][m].  Returns S~_k.
 template <class M>
-double rollout_one(const oracle_problem* pb, const double* Lsc /* sqrt(nu) L */,
+double rollout_one(const oracle_problem* pb, const double* Lsc /* L = chol(Sigma_u) */,
                    const double* x0, const double* U, const float* eps, int64_t K, int64_t k,
                    int* crashed_out, double* qstep = nullptr /* [T]: q~ of each step, or null */) {
     typedef typename M::S S;
     const int n = pb->n, m = pb->m, T = pb->T;
     S x[16];
     for (int i = 0; i < n; ++i) x[i] = (S)x0[i];
-    S Lt[16], Rt[16];
-    for (int i = 0; i < m * m; ++i) { Lt[i] = (S)Lsc[i]; Rt[i] = (S)pb->R[i]; }
-    const S c1 = (S)(0.5 * (1.0 - 1.0 / pb->nu));  // (1 - 1/nu)/2
+    S Rt[16];
+    for (int i = 0; i < m * m; ++i) Rt[i] = (S)pb->R[i];
     int crashed = 0;
     S Stilde = 0;
     for (int t = 0; t < T; ++t) {
+        // F_t = A_t L, Gi_t = Gamma~_t^{-1}; special case A = sqrt(nu) I: F = sqrt(nu) L and
+        // Gi = (1 - 1/nu) R, whose half is the (1 - 1/nu)/2 of PAPER.md:330
+        double Fd[16], Gd[16];
+        step_matrices(pb, t, Lsc, Fd, Gd);
+        S Ft[16], Gt[16];
+        for (int i = 0; i < m * m; ++i) { Ft[i] = (S)Fd[i]; Gt[i] = (S)Gd[i]; }
         const float* e = eps + ((int64_t)t * K + k) * m;
         S du[4], u[4], v[4];
-        for (int i = 0; i < m; ++i) {                 // du = sqrt(nu) L eps
+        for (int i = 0; i < m; ++i) {                 // du = A_t L eps
             S acc = 0;
-            for (int j = 0; j <= i; ++j) acc += Lt[i * m + j] * (S)e[j];
+            for (int j = 0; j < m; ++j) acc += Ft[i * m + j] * (S)e[j];
             du[i] = acc;
             u[i] = (S)U[t * m + i];
             v[i] = u[i] + du[i];                      // u_i + du_{i,k}
         }
         S q = plant_step<M>(pb, x, v, &crashed);      // x_{t+1}, q(x_{t+1})
-        S duRdu = 0, uRdu = 0, uRu = 0;
+        S duGdu = 0, uRdu = 0, uRu = 0;
         for (int i = 0; i < m; ++i)
             for (int j = 0; j < m; ++j) {
-                duRdu += du[i] * Rt[i * m + j] * du[j];
+                duGdu += du[i] * Gt[i * m + j] * du[j];
                 uRdu += u[i] * Rt[i * m + j] * du[j];
                 uRu += u[i] * Rt[i * m + j] * u[j];
             }
-        // q~ = q + (1-1/nu)/2 du'R du + u'R du + 1/2 u'R u
-        S qt = q + c1 * duRdu + uRdu + (S)0.5 * uRu;
+        // q~ = q + 1/2 du'Gamma~^{-1} du + u'R du + 1/2 u'R u
+        S qt = q + (S)0.5 * duGdu + uRdu + (S)0.5 * uRu;
         Stilde += qt;                                 // S~ += q~  (no dt: A2)
         if (qstep) qstep[t] = (double)qt;
     }
@@ -599,10 +655,14 @@ int oracle_rollout_costs(const oracle_problem* pb, const double* x0, const doubl
                          const float* eps, int64_t K, int32_t mode, int32_t nthreads,
                          double* costs, int32_t* crashed) {
     if (!problem_ok(pb) || K < 0) return 1;
-    double L[16], Lsc[16];
+    double L[16];
     if (!cholesky(pb->Sigma, pb->m, L)) return 2;
-    const double s = std::sqrt(pb->nu);
-    for (int i = 0; i < pb->m * pb->m; ++i) Lsc[i] = s * L[i];
+    if (pb->At) {
+        double F[16], G[16];
+        for (int t = 0; t < pb->T; ++t)
+            if (!step_matrices(pb, t, L, F, G)) return 3;       // singular A_t
+    }
+    const double* Lsc = L;
 #ifdef _OPENMP
     int nt = nthreads > 0 ? nthreads : omp_get_max_threads();
 #pragma omp parallel for num_threads(nt) schedule(static)
@@ -630,7 +690,6 @@ int oracle_update(const oracle_problem* pb, const double* costs, const float* ep
     const int m = pb->m, T = pb->T;
     double L[16];
     if (!cholesky(pb->Sigma, m, L)) return 2;
-    const double s = std::sqrt(pb->nu);
     double smin = costs[0];
     int64_t kstar = 0;
     for (int64_t k = 1; k < K; ++k)
@@ -643,12 +702,14 @@ int oracle_update(const oracle_problem* pb, const double* costs, const float* ep
     }
     const double etav = eta.value();
     for (int t = 0; t < T; ++t) {
+        double F[16], G[16];
+        step_matrices(pb, t, L, F, G);
         for (int i = 0; i < m; ++i) {
             NeumaierSum num;
             for (int64_t k = 0; k < K; ++k) {
                 const float* e = eps + ((int64_t)t * K + k) * m;
-                double du = 0.0;
-                for (int j = 0; j <= i; ++j) du += s * L[i * m + j] * (double)e[j];
+                double du = 0.0;                       // du = A_t L eps (default sqrt(nu) L eps)
+                for (int j = 0; j < m; ++j) du += F[i * m + j] * (double)e[j];
                 num.add(w[k] * du);
             }
             U[t * m + i] += num.value() / etav;
@@ -665,10 +726,9 @@ int oracle_update(const oracle_problem* pb, const double* costs, const float* ep
 int oracle_rollout_stepcosts(const oracle_problem* pb, const double* x0, const double* U,
                              const float* eps, int64_t K, int32_t nthreads, double* out, int32_t mode) {
     if (!problem_ok(pb) || K < 0) return 1;
-    double L[16], Lsc[16];
+    double L[16];
     if (!cholesky(pb->Sigma, pb->m, L)) return 2;
-    const double s = std::sqrt(pb->nu);
-    for (int i = 0; i < pb->m * pb->m; ++i) Lsc[i] = s * L[i];
+    const double* Lsc = L;
 #ifdef _OPENMP
     int nt = nthreads > 0 ? nthreads : omp_get_max_threads();
 #pragma omp parallel for num_threads(nt) schedule(static)
@@ -694,7 +754,6 @@ int oracle_update_ctg(const oracle_problem* pb, const double* stepcosts, const f
     const int m = pb->m, T = pb->T;
     double L[16];
     if (!cholesky(pb->Sigma, m, L)) return 2;
-    const double s = std::sqrt(pb->nu);
     std::vector<double> ctg((size_t)K * T);
     for (int64_t k = 0; k < K; ++k) {
         NeumaierSum acc;
@@ -713,12 +772,14 @@ int oracle_update_ctg(const oracle_problem* pb, const double* stepcosts, const f
             w[k] = std::exp(-(ctg[(size_t)k * T + t] - smin) / pb->lambda);
             eta.add(w[k]);
         }
+        double F[16], G[16];
+        step_matrices(pb, t, L, F, G);
         for (int i = 0; i < m; ++i) {
             NeumaierSum num;
             for (int64_t k = 0; k < K; ++k) {
                 const float* e = eps + ((int64_t)t * K + k) * m;
                 double du = 0.0;
-                for (int j = 0; j <= i; ++j) du += s * L[i * m + j] * (double)e[j];
+                for (int j = 0; j < m; ++j) du += F[i * m + j] * (double)e[j];
                 num.add(w[k] * du);
             }
             U[t * m + i] += num.value() / eta.value();
@@ -750,17 +811,18 @@ int oracle_trajectory(const oracle_problem* pb, const double* x0, const double* 
     if (!problem_ok(pb)) return 1;
     double L[16];
     if (!cholesky(pb->Sigma, pb->m, L)) return 2;
-    const double s = std::sqrt(pb->nu);
     const int n = pb->n, m = pb->m;
     double x[16];
     for (int i = 0; i < n; ++i) { x[i] = x0[i]; xs[i] = x[i]; }
     int crashed = 0;
     for (int t = 0; t < pb->T; ++t) {
         const float* e = eps + ((int64_t)t * K + k) * m;
+        double F[16], G[16];
+        step_matrices(pb, t, L, F, G);
         double v[4];
         for (int i = 0; i < m; ++i) {
             double du = 0;
-            for (int j = 0; j <= i; ++j) du += s * L[i * m + j] * (double)e[j];
+            for (int j = 0; j < m; ++j) du += F[i * m + j] * (double)e[j];
             v[i] = U[t * m + i] + du;
         }
         plant_step<MathD>(pb, x, v, &crashed);

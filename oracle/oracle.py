@@ -58,7 +58,7 @@ class _Problem(C.Structure):
                 ("Sigma", C.POINTER(C.c_double)), ("R", C.POINTER(C.c_double)),
                 ("params", C.POINTER(C.c_double)), ("n_params", C.c_int32),
                 ("n_obstacles", C.c_int32), ("obstacles", C.POINTER(C.c_double)),
-                ("penalty", C.c_double)]
+                ("penalty", C.c_double), ("At", C.POINTER(C.c_double))]
 
 
 _LIB = None
@@ -114,7 +114,7 @@ class Problem:
     """One MPPI problem (Alg. 1 "Given" block) for the oracle."""
 
     def __init__(self, plant, T, dt, lam, nu, Sigma, R, params=None, obstacles=None,
-                 n=None, m=None, penalty=1e30):
+                 n=None, m=None, penalty=1e30, At=None):
         self.plant = plant
         self.plant_id = PLANT_IDS[plant]
         if plant == "linear":
@@ -131,10 +131,14 @@ class Problem:
         obs = np.zeros((0, 2)) if obstacles is None else np.asarray(obstacles, np.float64)
         self.obstacles = np.ascontiguousarray(obs.reshape(-1, 2))
         self.penalty = float(penalty)
+        # NEXT-3: per-step sampling transforms A_t [T][m][m] (None: A_t = sqrt(nu) I)
+        self.At = None if At is None else np.ascontiguousarray(
+            np.asarray(At, np.float64).reshape(self.T, self.m, self.m))
         self._s = _Problem(self.plant_id, self.n, self.m, self.T, self.dt, self.lam, self.nu,
                            _dp(self.Sigma), _dp(self.R), _dp(self.params), len(self.params),
                            len(self.obstacles),
-                           _dp(self.obstacles) if len(self.obstacles) else None, self.penalty)
+                           _dp(self.obstacles) if len(self.obstacles) else None, self.penalty,
+                           _dp(self.At) if self.At is not None else None)
 
     def ptr(self):
         return C.byref(self._s)
