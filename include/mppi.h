@@ -297,6 +297,20 @@ mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, floa
  * order j = 0..i, U[t][i] = fl(U[t][i] + fl(d_i / eta)). */
 mppi_status_t mppi_apply(mppi_ctx* ctx, float* U, const float* buf);
 
+/* ---------------------------------------------------------------- general variance transform (NEXT-3) */
+
+/* mppi_set_sampling_transform — per-step variance transforms A_t of Theorem 1 (PAPER.md:177-201,
+ * B_E = A_t B_c), replacing the special case A = sqrt(nu) I.  With Eq. 7 in control
+ * coordinates (Sigma~ = R^{-1}, Lambda~_t = A_t R^{-1} A_t^T) the step samples
+ *   du_t = A_t L eps,  L = chol(Sigma)
+ * and charges  q~ = q + 1/2 du'(R - A_t^{-T} R A_t^{-1}) du + U_t'R du + 1/2 U_t'R U_t
+ * (for A_t = sqrt(nu) I exactly the (1 - 1/nu)/2 of PAPER.md:330); the update is
+ * U_t += A_t L A[t] / eta.  nu is then unused.
+ *   A : HOST fp64 [T][m][m] row-major, each A_t invertible (else INVALID_ARG); copied.  NULL
+ *       restores A_t = sqrt(nu) I.
+ * Synchronises the stream.  Uses the general (dense m x m) rollout path. */
+mppi_status_t mppi_set_sampling_transform(mppi_ctx* ctx, const double* A);
+
 /* ---------------------------------------------------------------- cost-to-go weights (NEXT-1) */
 
 typedef enum {

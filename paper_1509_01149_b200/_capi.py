@@ -96,7 +96,7 @@ KERNEL_NAMES = ["noise", "rollout", "wsum", "finalize", "shift"]
 EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize", "mppi_use_graph", "mppi_set_option",
            "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_apply",
            "mppi_shift", "mppi_noise", "mppi_feynman_kac", "mppi_closed_loop", "mppi_set_weighting",
-           "mppi_cost_to_go", "mppi_plant_step", "mppi_get_stats",
+           "mppi_cost_to_go", "mppi_set_sampling_transform", "mppi_plant_step", "mppi_get_stats",
            "mppi_last_launch_count", "mppi_profile_enable", "mppi_profile_read", "mppi_last_error", "mppi_status_string", "mppi_abi_version"]
 
 _lib = None
@@ -140,6 +140,8 @@ def lib():
     L.mppi_apply.restype = st
     L.mppi_shift.argtypes = [vp, vp, fp]
     L.mppi_shift.restype = st
+    L.mppi_set_sampling_transform.argtypes = [vp, dp]
+    L.mppi_set_sampling_transform.restype = st
     L.mppi_set_weighting.argtypes = [vp, C.c_int]
     L.mppi_set_weighting.restype = st
     L.mppi_cost_to_go.argtypes = [vp, vp]

@@ -69,7 +69,11 @@ struct Ctx {
     int64_t K = 0, K_loc = 0, k_offset = 0;
     int rank = 0, world = 1;
     float dt = 0, lambda = 0, nu = 1, c1 = 0, penalty = 1e30f;
-    bool diag = true;               // L and R both diagonal -> diagonal fast path
+    bool diag = true;               // L and R both diagonal -> diagonal fast path (and no A_t)
+    bool diag0 = true;              // the create-time value (restored when A_t is cleared)
+    bool per_t = false;             // NEXT-3: per-step transforms A_t set
+    float* d_mats = nullptr;        // [T][2][16] F_t = A_t L, G_t = (R - A_t^-T R A_t^-1) / 2
+    double L64[16] = {0};           // chol(Sigma) fp64
     bool pack2 = true;              // quadrotor (diagonal): two samples per thread, FP32x2
     float sL[16] = {0};             // sqrt(nu) * chol(Sigma), fp32, row-major m x m
     float R[16] = {0};              // control cost, fp32

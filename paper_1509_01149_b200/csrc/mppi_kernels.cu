@@ -164,6 +164,7 @@ struct RolloutArgs {
     float x0[16];
     const float* x0_dev;    // device-resident x0 (closed loop) or nullptr: use x0[]
     float* qstep;           // [T][K_loc] per-step q~_{t,k} (cost-to-go weighting) or nullptr
+    const float* mats;      // general path: [T][2][16] = (F_t = A_t L, G_t = (R - A^-T R A^-1)/2) or nullptr
     PP P;
     float4 obs_k[kMaxStaticPairs];  // negated obstacle pairs again, in the parameter constant bank
 };
@@ -185,8 +186,17 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
     float4* sObs = smem4;
     StepRec* sRec = reinterpret_cast<StepRec*>(smem4 + a.n_obs_pairs);   // per-t constants [T]
     float* sRing = reinterpret_cast<float*>(sRec + a.T);               // eps ring [2][blockDim][M]
+    // general path: per-t sampling factor F_t and IS matrix G_t after the ring ([T][2][M*M])
+    float* sMat = sRing + 2 * blockDim.x * M;
     const int tid = threadIdx.x;
     for (int i = tid; i < a.n_obs_pairs; i += blockDim.x) sObs[i] = a.obs[i];
+    if (!DIAG) {
+        for (int o = tid; o < a.T * 2 * M * M; o += blockDim.x) {
+            const int t = o / (2 * M * M), r = o % (2 * M * M), which = r / (M * M), ij = r % (M * M);
+            // default transform A = sqrt(nu) I: F = sqrt(nu) L, G = (1 - 1/nu)/2 R
+            sMat[o] = a.mats ? a.mats[t * 32 + which * 16 + ij] : (which == 0 ? a.sL[ij] : a.c1 * a.R[ij]);
+        }
+    }
     for (int t = tid; t < a.T; t += blockDim.x) {
         float u[4] = {0.0f, 0.0f, 0.0f, 0.0f}, bq[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
@@ -233,23 +243,26 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
                     is = fmaf(e[i], fmaf(a.ad[i], e[i], bb[i]), is);   // IS_t
                 }
             } else {
+                // du = F_t eps (F_t = A_t L, NEXT-3; default sqrt(nu) L), IS_t = du'G_t du + (R U_t).du + K_t
+                const float* F = sMat + t * 2 * M * M;
+                const float* G = F + M * M;
                 float du[M];
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
                     float d = 0.0f;
 #pragma unroll
-                    for (int j = 0; j <= i; ++j) d = fmaf(a.sL[i * M + j], e[j], d);
+                    for (int j = 0; j < M; ++j) d = fmaf(F[i * M + j], e[j], d);
                     du[i] = d;
                     v[i] = uu[i] + d;
                 }
-                float duRdu = 0.0f, uRdu = 0.0f;
+                float duGdu = 0.0f, uRdu = 0.0f;
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
 #pragma unroll
-                    for (int j = 0; j < M; ++j) duRdu = fmaf(du[i] * a.R[i * M + j], du[j], duRdu);
+                    for (int j = 0; j < M; ++j) duGdu = fmaf(du[i] * G[i * M + j], du[j], duGdu);
                     uRdu = fmaf(bb[i], du[i], uRdu);
                 }
-                is = fmaf(a.c1, duRdu, uRdu + is);
+                is = duGdu + (uRdu + is);
             }
             // rotated step: q(x_t) (the cost of step t-1, 0 at t = 0) and F(x_t, v_t) only need
             // x_t, so they share one basic block; then x_{t+1} = x_t + F dt
@@ -514,6 +527,7 @@ struct FinalizeArgs {
     DeviceStats* stats;
     int T, M;
     float sL[16];
+    const float* mats;     // per-t F_t (NEXT-3) or nullptr: U_t += sL A_t / eta
 };
 
 __global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeArgs a) {
@@ -542,7 +556,12 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeArgs a) {
         for (int o = threadIdx.x; o < TM; o += blockDim.x) {
             const int t = o / a.M, i = o % a.M;
             float d = 0.0f;  // d_i = sum_{j<=i} sL[i][j] A[t][j], explicit rounding order
-            for (int j = 0; j <= i; ++j) d = __fadd_rn(d, __fmul_rn(a.sL[i * a.M + j], sA[1 + t * a.M + j]));
+            if (a.mats) {    // general transform: d = F_t A_t (all j)
+                for (int j = 0; j < a.M; ++j)
+                    d = __fadd_rn(d, __fmul_rn(a.mats[t * 32 + i * a.M + j], sA[1 + t * a.M + j]));
+            } else {
+                for (int j = 0; j <= i; ++j) d = __fadd_rn(d, __fmul_rn(a.sL[i * a.M + j], sA[1 + t * a.M + j]));
+            }
             a.U[o] = __fadd_rn(a.U[o], __fdiv_rn(d, eta));   // U_t += sum w du / eta
         }
     }
@@ -698,6 +717,7 @@ struct FinalizeCtgArgs {
     DeviceStats* stats;
     int T, M;
     float sL[16];
+    const float* mats;
 };
 
 __global__ void __launch_bounds__(1024) finalize_ctg_kernel(const FinalizeCtgArgs a) {
@@ -707,10 +727,12 @@ __global__ void __launch_bounds__(1024) finalize_ctg_kernel(const FinalizeCtgArg
         float eta = 0.0f;
         for (int c = 0; c < a.n_chunks; ++c) eta += a.eta_part[(size_t)c * a.T + t];
         float d = 0.0f;
-        for (int j = 0; j <= i; ++j) {
+        const int jmax = a.mats ? a.M - 1 : i;
+        for (int j = 0; j <= jmax; ++j) {
             float A = 0.0f;
             for (int c = 0; c < a.n_chunks; ++c) A += a.part[((size_t)c * a.T + t) * a.M + j];
-            d = __fadd_rn(d, __fmul_rn(a.sL[i * a.M + j], A));
+            const float f = a.mats ? a.mats[t * 32 + i * a.M + j] : a.sL[i * a.M + j];
+            d = __fadd_rn(d, __fmul_rn(f, A));
         }
         a.U[o] = __fadd_rn(a.U[o], __fdiv_rn(d, eta));
         if (o == 0 && a.stats) a.stats->eta = eta;
@@ -766,6 +788,7 @@ cudaError_t launch_finalize_ctg(Ctx& c, float* U) {
     a.T = c.T;
     a.M = c.m;
     for (int i = 0; i < 16; ++i) a.sL[i] = c.sL[i];
+    a.mats = c.per_t ? c.d_mats : nullptr;
     const int threads = c.T * c.m >= 1024 ? 1024 : ((c.T * c.m + 31) / 32) * 32;
     return emit(c, (const void*)finalize_ctg_kernel, dim3(1), dim3(threads), 0, &a, sizeof(a),
                 MPPI_KERNEL_FINALIZE);
@@ -1036,6 +1059,7 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     }
     a.x0_dev = nullptr;
     a.qstep = c.ctg ? c.d_ctg : nullptr;
+    a.mats = c.per_t ? c.d_mats : nullptr;
     if (c.x0_on_device) a.x0_dev = x0;
     else for (int i = 0; i < c.n && i < 16; ++i) a.x0[i] = x0[i];
     a.P = P;
@@ -1043,7 +1067,8 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
         a.obs_k[i] = i < c.n_obs_pairs ? c.obs_host[i] : make_float4(-1e15f, -1e15f, -1e15f, -1e15f);
     const int spt = X2 ? 2 : 1;                                      // samples per thread
     const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
-                        (size_t)2 * kRolloutThreads * spt * Plant::M * sizeof(float);
+                        (size_t)2 * kRolloutThreads * spt * Plant::M * sizeof(float) +
+                        (DIAG ? 0 : (size_t)c.T * 2 * Plant::M * Plant::M * sizeof(float));
     const void* kern;
     if constexpr (X2) kern = (const void*)rollout_kernel_x2<NP>;
     else kern = (const void*)rollout_kernel<Plant, DIAG, NP>;
@@ -1151,6 +1176,7 @@ cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* 
     a.T = c.T;
     a.M = c.m;
     for (int i = 0; i < 16; ++i) a.sL[i] = c.sL[i];
+    a.mats = c.per_t ? c.d_mats : nullptr;
     const size_t smem = (size_t)(c.T * c.m + 1) * sizeof(float);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

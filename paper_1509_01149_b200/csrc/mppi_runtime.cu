@@ -78,6 +78,12 @@ int plant_control_dim(int plant) {
     }
 }
 
+bool all_finite_d(const double* p, int n) {
+    for (int i = 0; i < n; ++i)
+        if (!std::isfinite(p[i])) return false;
+    return true;
+}
+
 bool all_finite(const float* p, int n) {
     for (int i = 0; i < n; ++i)
         if (!isfinite(p[i])) return false;
@@ -208,6 +214,7 @@ void free_ctx(Ctx& c) {
     cudaFree(c.d_U);
     cudaFree(c.d_fk);
     cudaFree(c.d_ctg);
+    cudaFree(c.d_mats);
     cudaFree(c.d_ctg_partmin);
     cudaFree(c.d_ctg_smin);
     cudaFree(c.d_ctg_eta);
@@ -347,6 +354,8 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
             if (i != j && (L[i * m + j] != 0.0 || R[i * m + j] != 0.0)) diag = false;
         }
     c.diag = diag;
+    c.diag0 = diag;
+    for (int i = 0; i < m * m; ++i) c.L64[i] = L[i];
     for (int i = 0; i < m; ++i)   // IS_t = K_t + sum_i e_i (a_i e_i + b_ti) on the diagonal path
         c.ad[i] = (float)(0.5 * (1.0 - 1.0 / (double)nu) * R[i * m + i] * (s * L[i * m + i]) * (s * L[i * m + i]));
     mppi_status_t st = digest_params(c, dynamics, cost);
@@ -553,6 +562,70 @@ mppi_status_t mppi_set_weighting(mppi_ctx* ctx, mppi_weighting_t mode) {
     MPPI_CUDA(cudaStreamSynchronize(c.stream), "stream sync");
     c.ctg = mode == MPPI_WEIGHTS_COST_TO_GO;
     free_graphs(c);     // the step's kernel sequence changed
+    return MPPI_OK;
+}
+
+// fp64 Gauss-Jordan inverse (partial pivoting); false if singular
+static bool invert64(const double* A, int m, double* Ai) {
+    double a[16], b[16];
+    for (int i = 0; i < m * m; ++i) { a[i] = A[i]; b[i] = 0.0; }
+    for (int i = 0; i < m; ++i) b[i * m + i] = 1.0;
+    for (int col = 0; col < m; ++col) {
+        int p = col;
+        for (int r = col + 1; r < m; ++r)
+            if (fabs(a[r * m + col]) > fabs(a[p * m + col])) p = r;
+        if (!(fabs(a[p * m + col]) > 0.0)) return false;
+        for (int j = 0; j < m; ++j) {
+            double tmp = a[col * m + j]; a[col * m + j] = a[p * m + j]; a[p * m + j] = tmp;
+            tmp = b[col * m + j]; b[col * m + j] = b[p * m + j]; b[p * m + j] = tmp;
+        }
+        const double d = a[col * m + col];
+        for (int j = 0; j < m; ++j) { a[col * m + j] /= d; b[col * m + j] /= d; }
+        for (int r = 0; r < m; ++r) {
+            if (r == col) continue;
+            const double f = a[r * m + col];
+            for (int j = 0; j < m; ++j) { a[r * m + j] -= f * a[col * m + j]; b[r * m + j] -= f * b[col * m + j]; }
+        }
+    }
+    for (int i = 0; i < m * m; ++i) Ai[i] = b[i];
+    return true;
+}
+
+mppi_status_t mppi_set_sampling_transform(mppi_ctx* ctx, const double* A) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    MPPI_CUDA(cudaStreamSynchronize(c.stream), "stream sync");
+    free_graphs(c);     // the step's kernels change
+    if (!A) {
+        c.per_t = false;
+        c.diag = c.diag0;
+        return MPPI_OK;
+    }
+    const int m = c.m;
+    std::vector<float> mats((size_t)c.T * 32, 0.0f);
+    double Rd[16];
+    for (int i = 0; i < m * m; ++i) Rd[i] = (double)c.R[i];
+    for (int t = 0; t < c.T; ++t) {
+        const double* At = A + (size_t)t * m * m;
+        if (!all_finite_d(At, m * m)) return fail(MPPI_ERR_INVALID_ARG, "A_%d must be finite", t);
+        double Ai[16];
+        if (!invert64(At, m, Ai)) return fail(MPPI_ERR_INVALID_ARG, "A_%d is singular (Theorem 1 needs A_t invertible)", t);
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < m; ++j) {
+                double f = 0.0, g = 0.0;
+                for (int k = 0; k < m; ++k) f += At[i * m + k] * c.L64[k * m + j];
+                for (int k = 0; k < m; ++k)
+                    for (int l = 0; l < m; ++l) g += Ai[k * m + i] * Rd[k * m + l] * Ai[l * m + j];
+                mats[(size_t)t * 32 + i * m + j] = (float)f;
+                mats[(size_t)t * 32 + 16 + i * m + j] = (float)(0.5 * (Rd[i * m + j] - g));
+            }
+    }
+    if (!c.d_mats) {
+        if (mppi_status_t a = dalloc(c, &c.d_mats, (size_t)c.T * 32, "sampling transforms")) return a;
+    }
+    MPPI_CUDA(cudaMemcpy(c.d_mats, mats.data(), mats.size() * sizeof(float), cudaMemcpyHostToDevice), "A_t upload");
+    c.per_t = true;
+    c.diag = false;
     return MPPI_OK;
 }
 

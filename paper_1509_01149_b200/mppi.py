@@ -167,6 +167,14 @@ class MPPI:
         A.check(self.lib.mppi_noise(self.ctx, seed, step, _fptr(out)))
         return out
 
+    def set_sampling_transform(self, At=None):
+        """mppi_set_sampling_transform: per-step A_t [T][m][m] (fp64, Theorem 1) or None for sqrt(nu) I."""
+        if At is None:
+            A.check(self.lib.mppi_set_sampling_transform(self.ctx, None))
+            return
+        self._At = np.ascontiguousarray(np.asarray(At, np.float64).reshape(self.T, self.m, self.m))
+        A.check(self.lib.mppi_set_sampling_transform(self.ctx, self._At.ctypes.data_as(C.POINTER(C.c_double))))
+
     def set_weighting(self, cost_to_go):
         """mppi_set_weighting: per-timestep cost-to-go weights or trajectory."""
         A.check(self.lib.mppi_set_weighting(
