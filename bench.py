@@ -57,6 +57,9 @@ def parse_args():
     p.add_argument("--no-probe", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-extra", action="store_true", help="skip the C3/C4/K-sweep/closed-loop extras")
+    p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                   help="process-group backend for N > 1 (gloo: a CPU-side test of the sharded path "
+                        "that lets several ranks share one GPU)")
     return p.parse_args()
 
 
@@ -339,9 +342,13 @@ def main():
     from mppi_inputs import get
     from paper_1509_01149_b200 import ShardedMPPI, from_workload
 
-    torch.cuda.set_device(local)
+    dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     w = get(args.config)
     K = args.K or w.K
     m = from_workload(w, K=K, rank=rank, world=world)
@@ -359,7 +366,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev)
     clocks.start()
     m.profile_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -427,7 +434,7 @@ def main():
 
     # ---- roofline of the dominant kernel (rank 0's launches, CUDA events on its stream)
     pk = measured_peaks()
-    props = torch.cuda.get_device_properties(local)
+    props = torch.cuda.get_device_properties(dev)
     sm_max = (clk or {}).get("sm_max_mhz") or pk.get("sm_max_mhz", 1965.0)
     kern = {k: {"avg_ms": v[0] / v[1] if v[1] else None, "launches": v[1], "share": None}
             for k, v in ktimes.items()}
@@ -497,7 +504,8 @@ def main():
                    "parallelism": "K-sharded dp%d, NCCL MIN + SUM allreduce" % world},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk, "kernels": kern, "latency": lat, "extra": extra,
-        "device": torch.cuda.get_device_name(local),
+        "device": torch.cuda.get_device_name(dev),
+        "backend": args.backend if world > 1 else None,
     }
     print(json.dumps(line), flush=True)
     m.close()
