@@ -353,7 +353,12 @@ def main():
     K = args.K or w.K
     m = from_workload(w, K=K, rank=rank, world=world)
     U = torch.tensor(w.U0, device="cuda")
-    sh = ShardedMPPI(m) if world > 1 else None
+    # NCCL: the library drives both collectives itself on its stream (mppi_nccl_attach); gloo (a
+    # CPU-side check of the same sharded path): the split-phase calls + torch.distributed
+    lib_nccl = world > 1 and args.backend == "nccl"
+    if lib_nccl:
+        m.attach_nccl()
+    sh = ShardedMPPI(m) if world > 1 and not lib_nccl else None
 
     def step(i, Ut):
         if sh is None:
@@ -401,13 +406,19 @@ def main():
         Uh = np.ascontiguousarray(w.U0.copy())
         h2d = w.T * w.m * 4 + w.n * 4
         d2h = w.T * w.m * 4
-        if world == 1:
+        if sh is None:
+            if world > 1:
+                dist.barrier()
             for i in range(2):
                 m.optimize_host(w.x0, Uh, w.seed, i)
             t0 = time.perf_counter()
             for i in range(args.steps):
                 m.optimize_host(w.x0, Uh, w.seed, args.warmup + i)
             el = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([el], device="cuda", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                el = float(t.item())
         else:
             Up = torch.tensor(w.U0).pin_memory()
             Ud = torch.empty_like(U)
@@ -424,7 +435,7 @@ def main():
             el = float(t.item())
         e2e = {"value": K * w.T * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * el / args.steps,
-               "api": "mppi_optimize_host" if world == 1 else "ShardedMPPI.optimize + pinned copies"}
+               "api": "mppi_optimize_host" if sh is None else "ShardedMPPI.optimize + pinned copies"}
 
     if rank != 0:
         m.close()
@@ -501,7 +512,9 @@ def main():
                    % (args.config, w.plant, K, w.T, w.m, w.nu, w.lam),
                    "K": K, "K_per_gpu": K_loc, "T": w.T, "n_obstacles": int(len(w.obstacles)),
                    "l2": "inputs larger than L2 (noise %.1f GB per GPU per step)" % (eps_bytes / 1e9),
-                   "parallelism": "K-sharded dp%d, NCCL MIN + SUM allreduce" % world},
+                   "parallelism": "K-sharded dp%d, %s" % (world, "single GPU" if world == 1 else
+                                                          "in-library NCCL MIN + SUM allreduce" if lib_nccl else
+                                                          "MIN + SUM allreduce via torch.distributed")},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk, "kernels": kern, "latency": lat, "extra": extra,
         "device": torch.cuda.get_device_name(dev),

@@ -46,6 +46,7 @@ typedef enum {
     MPPI_ERR_NOT_SPD = 2,      /* Sigma or R is not symmetric positive definite (fp64 Cholesky) */
     MPPI_ERR_OOM = 3,          /* device or pinned-host allocation failed */
     MPPI_ERR_CUDA = 4,         /* CUDA runtime error (no device, launch failure, async fault) */
+    MPPI_ERR_NCCL = 5,         /* NCCL unavailable or a collective failed */
     MPPI_ERR_UNSUPPORTED = 6   /* valid request outside what this build implements */
 } mppi_status_t;
 
@@ -237,7 +238,8 @@ mppi_status_t mppi_set_stream(mppi_ctx* ctx, void* cuda_stream);
 
 /* ---------------------------------------------------------------- the step */
 
-/* mppi_optimize — one full MPPI step, world == 1 only (else UNSUPPORTED):
+/* mppi_optimize — one full MPPI step.  world == 1, or world > 1 with a communicator attached by
+ * mppi_nccl_attach (else UNSUPPORTED; the split-phase calls below work without one):
  *   noise -> rollout -> min -> weights + weighted noise sum -> U update.
  *   x0    : HOST float [n], the current state x_{t0}; read before return (passed by value).
  *   U     : DEVICE float [T][m], the nominal control sequence, updated in place.
@@ -271,6 +273,25 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
  * SYNCHRONOUS (returns after U is in host memory).  U: HOST float [T][m] in/out. */
 mppi_status_t mppi_optimize_host(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed,
                                  uint64_t step);
+
+/* ---------------------------------------------------------------- NCCL (multi-GPU, row e) */
+
+#define MPPI_NCCL_ID_BYTES 128
+
+/* mppi_nccl_unique_id — a fresh NCCL unique id (HOST uint8 [128]); call on one rank and hand the
+ * bytes to every rank (e.g. torch.distributed broadcast).  NCCL is the libnccl.so.2 the process
+ * already loaded (torch's), resolved at run time.  Errors: NCCL. */
+mppi_status_t mppi_nccl_unique_id(uint8_t* id);
+
+/* mppi_nccl_attach — COLLECTIVE over the context's world (every rank calls it with the same id;
+ * blocks until all joined): creates the communicator the library uses from then on, so that
+ * mppi_optimize runs the whole K-sharded step on the context stream:
+ *   rollouts of this rank's K/world samples -> ncclAllReduce(MIN) of the int64 (cost, k) key
+ *   (8 B) -> local weights and weighted noise sums -> ncclAllReduce(SUM) of [eta, A] ((1+T m) fp32)
+ *   -> the same U update on every rank (U stays a bit-identical replica).
+ * A single-rank communicator (world == 1) is allowed (the collectives are identities).
+ * The cost-to-go weighting is not supported with a communicator in this version. */
+mppi_status_t mppi_nccl_attach(mppi_ctx* ctx, const uint8_t* id);
 
 /* ---------------------------------------------------------------- split phase (multi-GPU) */
 

@@ -11,6 +11,8 @@ LIB_PATH = os.path.join(HERE, "libmppi_b200.so")
 
 MPPI_OK, MPPI_ERR_INVALID_ARG, MPPI_ERR_NOT_SPD, MPPI_ERR_OOM, MPPI_ERR_CUDA, MPPI_ERR_UNSUPPORTED = \
     0, 1, 2, 3, 4, 6
+MPPI_ERR_NCCL = 5
+MPPI_NCCL_ID_BYTES = 128
 MPPI_PLANT_CARTPOLE, MPPI_PLANT_RACECAR, MPPI_PLANT_QUADROTOR, MPPI_PLANT_LINEAR = 1, 2, 3, 4
 MPPI_MAX_OBSTACLES = 4096
 MPPI_OPTION_CUDA_GRAPH, MPPI_OPTION_PACKED_SAMPLES = 1, 2
@@ -96,7 +98,7 @@ KERNEL_NAMES = ["noise", "rollout", "wsum", "finalize", "shift"]
 EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize", "mppi_use_graph", "mppi_set_option",
            "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_apply",
            "mppi_shift", "mppi_noise", "mppi_feynman_kac", "mppi_closed_loop", "mppi_set_weighting",
-           "mppi_cost_to_go", "mppi_set_sampling_transform", "mppi_plant_step", "mppi_get_stats",
+           "mppi_cost_to_go", "mppi_set_sampling_transform", "mppi_nccl_unique_id", "mppi_nccl_attach", "mppi_plant_step", "mppi_get_stats",
            "mppi_last_launch_count", "mppi_profile_enable", "mppi_profile_read", "mppi_last_error", "mppi_status_string", "mppi_abi_version"]
 
 _lib = None
@@ -140,6 +142,10 @@ def lib():
     L.mppi_apply.restype = st
     L.mppi_shift.argtypes = [vp, vp, fp]
     L.mppi_shift.restype = st
+    L.mppi_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+    L.mppi_nccl_unique_id.restype = st
+    L.mppi_nccl_attach.argtypes = [vp, C.POINTER(C.c_uint8)]
+    L.mppi_nccl_attach.restype = st
     L.mppi_set_sampling_transform.argtypes = [vp, dp]
     L.mppi_set_sampling_transform.restype = st
     L.mppi_set_weighting.argtypes = [vp, C.c_int]

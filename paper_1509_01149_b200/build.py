@@ -20,6 +20,18 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-cudart",
          "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 
+def nccl_include():
+    """nccl.h of the NCCL torch ships (types only; the library resolves NCCL at run time)."""
+    try:
+        import nvidia.nccl
+        d = os.path.join(list(nvidia.nccl.__path__)[0], "include")
+        if os.path.exists(os.path.join(d, "nccl.h")):
+            return d
+    except Exception:
+        pass
+    return "/usr/include"
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -41,7 +53,7 @@ def build(force=False, verbose=False):
         return LIB
     tmp = LIB + ".tmp%d" % os.getpid()
     cmd = [NVCC] + ARCH + FLAGS + ["-I", os.path.join(ROOT, "include"), "-I", CSRC,
-                                   "-shared", "-o", tmp] + sources()
+                                   "-I", nccl_include(), "-shared", "-o", tmp] + sources() + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

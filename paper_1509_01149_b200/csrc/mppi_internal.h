@@ -115,6 +115,9 @@ struct Ctx {
     bool x0_on_device = false;            // launch_rollout's x0 is a device pointer (closed loop)
     std::vector<KLaunch> pending;
     GraphState graphs[2];
+    // row (e): a communicator the library drives itself (mppi_nccl_attach)
+    void* nccl = nullptr;                 // ncclComm_t
+    float* d_commbuf = nullptr;           // [1 + T*m]: [eta, A] all-reduced across ranks
 };
 
 // Launch (or collect, see Ctx::collect) one kernel whose single parameter is `args`.
@@ -138,6 +141,14 @@ cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key);
 cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* U);
 cudaError_t launch_shift(Ctx& c, float* U, const float* u_init);
 int wsum_blocks_per_sm(int m);  // resident wsum CTAs per SM (occupancy API)
+// NCCL (mppi_nccl.cu): runtime-resolved, 0 on success, >0 ncclResult_t, -1 unavailable
+bool nccl_available();
+int nccl_unique_id(unsigned char* out);
+int nccl_attach(Ctx& c, const unsigned char* id_bytes);
+void nccl_detach(Ctx& c);
+const char* nccl_error(int r);
+int nccl_min_key(Ctx& c, long long* key);
+int nccl_sum_buf(Ctx& c, float* buf, size_t count);
 cudaError_t launch_fk_reduce(Ctx& c, double* part, int nblk);   // Feynman-Kac partial sums
 cudaError_t launch_ctg(Ctx& c);                                  // cost-to-go + per-t minima
 cudaError_t launch_wsum_ctg(Ctx& c, const float* eps);

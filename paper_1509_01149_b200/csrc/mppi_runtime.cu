@@ -200,6 +200,8 @@ void free_graphs(Ctx& c) {
 
 void free_ctx(Ctx& c) {
     free_graphs(c);
+    nccl_detach(c);
+    cudaFree(c.d_commbuf);
     for (auto& p : c.ev_pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
     for (auto e : c.ev_pool) cudaEventDestroy(e);
     c.ev_pending.clear();
@@ -283,6 +285,7 @@ const char* mppi_status_string(mppi_status_t s) {
         case MPPI_ERR_OOM: return "MPPI_ERR_OOM";
         case MPPI_ERR_CUDA: return "MPPI_ERR_CUDA";
         case MPPI_ERR_UNSUPPORTED: return "MPPI_ERR_UNSUPPORTED";
+        case MPPI_ERR_NCCL: return "MPPI_ERR_NCCL";
         default: return "MPPI_ERR_UNKNOWN";
     }
 }
@@ -531,11 +534,53 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
     }
 }
 
+// The K-sharded step with the library's communicator (row e): rollouts -> allreduce MIN of the
+// key -> local weights and weighted noise sums -> allreduce SUM of [eta, A] -> identical update
+// on every rank.  All on the context stream; direct launches.
+static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t seed, uint64_t step,
+                                   const float* noise) {
+    if (c.ctg) return fail(MPPI_ERR_UNSUPPORTED, "cost-to-go weighting with a communicator (round 1: world 1)");
+    c.last_launches = 0;
+    const float* eps = nullptr;
+    if (mppi_status_t s = do_rollout(c, x0, U, seed, step, noise, nullptr, &eps)) return s;
+    int r = nccl_min_key(c, &c.d_stats->min_key);
+    if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(MIN key): %s", nccl_error(r));
+    MPPI_CUDA(launch_wsum(c, eps, &c.d_stats->min_key), "wsum_kernel launch");
+    MPPI_CUDA(launch_finalize(c, nullptr, c.d_commbuf, nullptr), "finalize (partials) launch");
+    r = nccl_sum_buf(c, c.d_commbuf, (size_t)1 + (size_t)c.T * c.m);
+    if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(SUM [eta, A]): %s", nccl_error(r));
+    MPPI_CUDA(launch_finalize(c, c.d_commbuf, nullptr, U), "finalize (apply) launch");
+    c.last_eps = eps;
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_nccl_unique_id(uint8_t* id) {
+    if (!id) return fail(MPPI_ERR_INVALID_ARG, "id is NULL");
+    const int r = nccl_unique_id(id);
+    if (r) return fail(MPPI_ERR_NCCL, "ncclGetUniqueId: %s", nccl_error(r));
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_nccl_attach(mppi_ctx* ctx, const uint8_t* id) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (!id) return fail(MPPI_ERR_INVALID_ARG, "id is NULL");
+    if (c.nccl) return fail(MPPI_ERR_INVALID_ARG, "a communicator is already attached");
+    if (!c.d_commbuf)
+        if (mppi_status_t a = dalloc(c, &c.d_commbuf, (size_t)1 + (size_t)c.T * c.m, "comm buffer")) return a;
+    const int r = nccl_attach(c, id);
+    if (r) return fail(MPPI_ERR_NCCL, "ncclCommInitRank(world %d, rank %d): %s", c.world, c.rank, nccl_error(r));
+    free_graphs(c);
+    return MPPI_OK;
+}
+
 mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed, uint64_t step,
                             const float* noise) {
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
-    if (c.world != 1) return fail(MPPI_ERR_UNSUPPORTED, "mppi_optimize needs world == 1; use the split-phase calls");
+    if (c.nccl) return optimize_nccl(c, x0, U, seed, step, noise);
+    if (c.world != 1) return fail(MPPI_ERR_UNSUPPORTED, "mppi_optimize with world > 1 needs mppi_nccl_attach "
+                                  "(or use the split-phase calls)");
     if (c.use_graph && !c.prof) return optimize_graph(c, x0, U, seed, step, noise);
     c.last_launches = 0;
     const float* eps = nullptr;

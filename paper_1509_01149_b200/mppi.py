@@ -167,6 +167,23 @@ class MPPI:
         A.check(self.lib.mppi_noise(self.ctx, seed, step, _fptr(out)))
         return out
 
+    def attach_nccl(self, group=None):
+        """mppi_nccl_attach: rank 0 draws an NCCL unique id, torch.distributed broadcasts it (when
+        initialised), every rank attaches; afterwards optimize() runs the whole sharded step."""
+        buf = (C.c_uint8 * A.MPPI_NCCL_ID_BYTES)()
+        import torch.distributed as dist
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+        rank = dist.get_rank(group) if multi else 0
+        if rank == 0:
+            A.check(self.lib.mppi_nccl_unique_id(buf))
+        if multi:
+            t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+            buf = (C.c_uint8 * A.MPPI_NCCL_ID_BYTES)(*t.cpu().tolist())
+        A.check(self.lib.mppi_nccl_attach(self.ctx, buf))
+
     def set_sampling_transform(self, At=None):
         """mppi_set_sampling_transform: per-step A_t [T][m][m] (fp64, Theorem 1) or None for sqrt(nu) I."""
         if At is None:

@@ -1,0 +1,58 @@
+"""Row (e) with the library's own communicator (mppi_nccl_attach, include/mppi.h): mppi_optimize
+runs rollouts -> ncclAllReduce(MIN key) -> weighted sums -> ncclAllReduce(SUM [eta, A]) -> update
+on the context stream.  One GPU here, so a single-rank communicator: the collectives are
+identities and the result must equal the direct single-GPU step bit for bit (same kernels, same
+reduction order).  The cross-rank arithmetic itself is covered by test_gpu_parity's sharding
+emulation and test_dist_gloo."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from mppi_inputs import get  # noqa: E402
+from paper_1509_01149_b200 import MppiError, from_workload  # noqa: E402
+
+
+@pytest.mark.parametrize("cfg,K", [("C1", 1024), ("C4", 65536)])
+def test_single_rank_nccl_equals_direct(cfg, K):
+    w = get(cfg)
+    a = from_workload(w, K=K)
+    b = from_workload(w, K=K)
+    b.attach_nccl()
+    Ua = torch.tensor(w.U0, device="cuda")
+    Ub = Ua.clone()
+    for i in range(3):
+        a.optimize(w.x0, Ua, w.seed, i)
+        b.optimize(w.x0, Ub, w.seed, i)
+    torch.cuda.synchronize()
+    assert torch.equal(Ua, Ub)
+    sa, sb = a.stats(), b.stats()
+    assert sa["k_star"] == sb["k_star"] and sa["s_min"] == sb["s_min"] and sa["eta"] == sb["eta"]
+    Uh = np.ascontiguousarray(w.U0.copy())
+    b.optimize_host(w.x0, Uh, w.seed, 0)
+    Ud = torch.tensor(w.U0, device="cuda")
+    a.optimize(w.x0, Ud, w.seed, 0)
+    assert np.array_equal(Uh, Ud.cpu().numpy())
+    a.close()
+    b.close()
+
+
+def test_world2_optimize_needs_communicator():
+    w = get("C1")
+    m = from_workload(w, K=1024, rank=0, world=2)
+    U = torch.tensor(w.U0, device="cuda")
+    with pytest.raises(MppiError):
+        m.optimize(w.x0, U, w.seed, 0)
+    m.close()
+
+
+def test_double_attach_rejected():
+    w = get("C1")
+    m = from_workload(w, K=1024)
+    m.attach_nccl()
+    with pytest.raises(MppiError):
+        m.attach_nccl()
+    m.close()
