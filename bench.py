@@ -32,6 +32,19 @@ UNIT = "K*T/s"
 # yet measured for that plant (roofline falls back to the kernel's measured share only).
 ROLLOUT_FLOP_PER_SS = {"cartpole": 59.43, "racecar": 251.49,  # profiles/r1_rollout_flops_*_v7.csv
                        "quadrotor": 464.56}  # profiles/r1_ncu_full_c5_v7.txt (rollout v7, x2)
+# The packed quadrotor rollout with the obstacle candidate grid and the in-kernel noise (the C5
+# path, K_loc >= 65536): FP32 FLOPs, issued thread instructions and DRAM bytes per sample-step,
+# ncu --set full at C5 (profiles/r1_ncu_full_c5_v8.txt).  The kernel also draws the noise
+# (Philox integer work, Box-Muller) so it is issue-bound on a mixed integer/FP32 stream; the
+# FP32-pipe fraction is the roofline, the issue-slot fraction is reported beside it.
+FUSED_QUAD = {"flop": 358.59, "inst": 369.43, "dram_bytes": 15.954}
+
+
+def rollout_variant(w, K_loc):
+    """Which rollout kernel bench.py's configuration runs (mirrors dispatch_np/fused_noise_applies)."""
+    if w.plant == "quadrotor" and K_loc >= 65536 and w.obstacles is not None and len(w.obstacles) >= 2:
+        return "x2-grid-fused"
+    return "scalar"
 
 SM_COUNT_B200 = 148
 FP32_LANES_PER_SM = 128
@@ -458,11 +471,19 @@ def main():
     roof = {"kernel": dom}
     if dom == "rollout":
         fp = fp32_peak(not args.no_probe, props.multi_processor_count, sm_max)
-        fl = ROLLOUT_FLOP_PER_SS.get(w.plant)
-        ach = fl * K_loc * w.T / avg_s / 1e12 if fl else None
+        variant = rollout_variant(w, K_loc)
+        fused = variant == "x2-grid-fused"
+        fl = FUSED_QUAD["flop"] if fused else ROLLOUT_FLOP_PER_SS.get(w.plant)
+        units = K_loc * w.T
+        ach = fl * units / avg_s / 1e12 if fl else None
         roof.update({"bound": "alu", "achieved": ach, "peak": fp["peak_tflops"], "unit": "TFLOP/s",
-                     "frac": ach / fp["peak_tflops"] if ach else None, "traffic": None,
-                     "flop_per_sample_step": fl, "peak_detail": fp})
+                     "frac": ach / fp["peak_tflops"] if ach else None,
+                     "traffic": FUSED_QUAD["dram_bytes"] * units if fused else None,
+                     "algorithmic_bytes_per_launch": 4.0 * w.m * units + 4.0 * K_loc if fused else None,
+                     "flop_per_sample_step": fl, "variant": variant, "peak_detail": fp})
+        if fused:   # issue-slot utilisation: 1 warp instruction / cycle / SM sub-partition
+            slots = props.multi_processor_count * 4 * sm_max * 1e6
+            roof["issue_frac"] = FUSED_QUAD["inst"] / 32.0 * units / avg_s / slots
     else:
         algo = 4.0 * w.T * K_loc * w.m + 4.0 * K_loc if dom == "wsum" else 4.0 * w.T * K_loc * w.m
         peak = pk.get("hbm_gbs", 6650.0)

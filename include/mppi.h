@@ -260,9 +260,18 @@ mppi_status_t mppi_use_graph(mppi_ctx* ctx, int32_t enable);
 
 typedef enum {
     MPPI_OPTION_CUDA_GRAPH = 1,        /* same as mppi_use_graph (default 1) */
-    MPPI_OPTION_PACKED_SAMPLES = 2     /* quadrotor, diagonal Sigma and R, K_loc >= 65536: two samples
+    MPPI_OPTION_PACKED_SAMPLES = 2,    /* quadrotor, diagonal Sigma and R, K_loc >= 65536: two samples
                                           per thread with FP32x2 arithmetic (default 1); bitwise
                                           identical results */
+    MPPI_OPTION_FUSED_NOISE = 3,       /* when the packed quadrotor rollout runs and the library draws
+                                          the noise: the rollout kernel draws it itself (same
+                                          counters, bit-identical values, still written to the
+                                          context's noise buffer for the reduction) instead of a
+                                          separate noise pass (default 1) */
+    MPPI_OPTION_OBSTACLE_GRID = 4      /* packed quadrotor rollout: the nearest cylinder is searched
+                                          among a per-cell candidate list (host-built at create)
+                                          instead of all cylinders; bitwise identical results
+                                          (default 1) */
 } mppi_option_t;
 
 /* mppi_set_option — execution options that never change results. */

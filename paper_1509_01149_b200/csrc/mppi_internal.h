@@ -75,12 +75,25 @@ struct Ctx {
     float* d_mats = nullptr;        // [T][2][16] F_t = A_t L, G_t = (R - A_t^-T R A_t^-1) / 2
     double L64[16] = {0};           // chol(Sigma) fp64
     bool pack2 = true;              // quadrotor (diagonal): two samples per thread, FP32x2
+    bool fuse_noise = true;         // packed rollout draws its own noise (no K1 pass)
+    // set around a fused launch: the rollout writes the noise it draws here (else nullptr)
+    float* gen_eps = nullptr;
+    uint64_t gen_seed = 0, gen_step = 0;
     float sL[16] = {0};             // sqrt(nu) * chol(Sigma), fp32, row-major m x m
     float R[16] = {0};              // control cost, fp32
     float ad[4] = {0};              // diagonal path: (1 - 1/nu)/2 R_ii (sqrt(nu) L_ii)^2
     PlantParamsU params;            // pre-digested plant/cost parameters
     std::vector<float4> obs_host;   // negated obstacle pairs (host copy, for mppi_plant_step)
     int n_obs_pairs = 0;
+    // nearest-cylinder candidate grid (quadrotor): cell words + negated centres, see build_cell_grid
+    std::vector<uint32_t> cells_host;
+    std::vector<float2> cent_host;
+    uint32_t* d_cells = nullptr;
+    float2* d_cent = nullptr;
+    int cell_nx = 0, cell_ny = 0;
+    float cell_ox = 0.0f, cell_oy = 0.0f, cell_inv_h = 0.0f;   // cell coord = p / h + o
+    bool use_cells = true;          // MPPI_OPTION_OBSTACLE_GRID (when a grid was built)
+    float cell_band = 0.0f;         // border cells extend this many cells outward
     // device workspace
     float4* d_obs = nullptr;
     float* d_eps = nullptr;         // [T][K_loc][m]
@@ -141,6 +154,7 @@ cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key);
 cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* U);
 cudaError_t launch_shift(Ctx& c, float* U, const float* u_init);
 int wsum_blocks_per_sm(int m);  // resident wsum CTAs per SM (occupancy API)
+bool fused_noise_applies(const Ctx& c);  // the rollout kernel for c can draw its own noise
 // NCCL (mppi_nccl.cu): runtime-resolved, 0 on success, >0 ncclResult_t, -1 unavailable
 bool nccl_available();
 int nccl_unique_id(unsigned char* out);

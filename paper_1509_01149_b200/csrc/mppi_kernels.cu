@@ -167,6 +167,15 @@ struct RolloutArgs {
     const float* mats;      // general path: [T][2][16] = (F_t = A_t L, G_t = (R - A^-T R A^-1)/2) or nullptr
     PP P;
     float4 obs_k[kMaxStaticPairs];  // negated obstacle pairs again, in the parameter constant bank
+    // nearest-cylinder candidate grid (NP == kCellGrid): staged into shared memory per CTA
+    const uint32_t* cells;
+    const float2* cent;
+    int cell_nx, cell_ny, n_cent;
+    float cell_ox, cell_oy, cell_inv_h, cell_band;
+    // fused noise (GEN kernels): eps[t][k] drawn in-kernel with the K1 counters and written here
+    float* eps_out;
+    unsigned step_lo, step_hi;
+    PhiloxKeys keys;
 };
 
 // One sample per thread.  Per step t:
@@ -317,7 +326,12 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
 // Quadrotor with diagonal L and R: two adjacent samples per thread (k = 2j, 2j+1), every FP32
 // operation packed as FP32x2 (QuadrotorX2), the obstacle-pair loads shared by both samples.
 // Same per-step arithmetic and the same (cost, k) key as rollout_kernel.
-template <int NP>
+//
+// GEN: the kernel draws eps[t][k], eps[t][k+1] itself (Philox counters (k_global, t, step), the
+// same packed Box-Muller as K1, so the values are bit-identical to K1's) one step ahead of their
+// use, and writes them to eps_out for K3; the noise pass and its HBM round trip disappear and the
+// integer/MUFU-heavy noise arithmetic fills issue slots the FMA-bound dynamics leaves idle.
+template <int NP, bool GEN>
 __global__ void __launch_bounds__(kRolloutThreads, 4)
     rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
     constexpr int M = 4;
@@ -325,8 +339,15 @@ __global__ void __launch_bounds__(kRolloutThreads, 4)
     float4* sObs = smem4;
     StepRec* sRec = reinterpret_cast<StepRec*>(smem4 + a.n_obs_pairs);
     float* sRing = reinterpret_cast<float*>(sRec + a.T);               // [2][blockDim][2 samples][4]
+    float2* sCent = reinterpret_cast<float2*>(sRing + (GEN ? 0 : 2 * kRolloutThreads * 2 * 4));
+    uint32_t* sCells = reinterpret_cast<uint32_t*>(sCent + a.n_cent);
     const int tid = threadIdx.x;
     for (int i = tid; i < a.n_obs_pairs; i += blockDim.x) sObs[i] = a.obs[i];
+    if constexpr (NP == kCellGrid) {
+        for (int i = tid; i < a.n_cent; i += blockDim.x) sCent[i] = a.cent[i];
+        const int nc = a.cell_nx * a.cell_ny;
+        for (int i = tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
+    }
     for (int t = tid; t < a.T; t += blockDim.x) {
         float u[4], bq[4];
         float kk = 0.0f;
@@ -353,7 +374,17 @@ __global__ void __launch_bounds__(kRolloutThreads, 4)
     if (k < a.K_loc) {
         QuadrotorX2 st;
         st.load(a.x0_dev ? a.x0_dev : a.x0);
-        const ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
+        ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
+        if constexpr (NP == kCellGrid) {
+            ob.cells = sCells;
+            ob.cent = sCent;
+            ob.nx = a.cell_nx;
+            ob.ny = a.cell_ny;
+            ob.ox = a.cell_ox;
+            ob.oy = a.cell_oy;
+            ob.inv_h = a.cell_inv_h;
+            ob.band = a.cell_band;
+        }
         const size_t row = (size_t)a.K_loc * M;
         V2 S = vb(0.0f);
         V2 is_prev = vb(0.0f);
@@ -361,21 +392,41 @@ __global__ void __launch_bounds__(kRolloutThreads, 4)
         const unsigned slot0 = (unsigned)__cvta_generic_to_shared(sRing + tid * 2 * M);
         const unsigned slot_sum = 2u * slot0 + blockDim.x * 2 * M * (unsigned)sizeof(float);
         unsigned cur = slot0;
-        cp_async_eps<4>(cur, gp);
-        cp_async_eps<4>(cur + 16, gp + 4);
-        cp_async_commit();
+        const unsigned kg = a.k_offset + (unsigned)k;
+        float4* op = GEN ? reinterpret_cast<float4*>(a.eps_out + (size_t)k * M) : nullptr;
+        float ga[4], gb[4];                                             // GEN: eps of step t
+        if constexpr (GEN) {
+            bm32_normals_x2<4>(philox4x32_10_dev(kg, 0u, a.step_lo, a.step_hi, a.keys),
+                               philox4x32_10_dev(kg + 1u, 0u, a.step_lo, a.step_hi, a.keys), ga, gb);
+        } else {
+            cp_async_eps<4>(cur, gp);
+            cp_async_eps<4>(cur + 16, gp + 4);
+            cp_async_commit();
+        }
         const StepRec* rec = sRec;
         for (int t = 0; t < a.T; ++t, ++rec) {
-            gp += row;
-            if (t + 1 < a.T) {
-                cp_async_eps<4>(slot_sum - cur, gp);
-                cp_async_eps<4>(slot_sum - cur + 16, gp + 4);
-            }
-            cp_async_commit();
-            cp_async_wait<1>();
             float ea[4], eb[4];
-            load_shared_eps<4>(cur, ea);
-            load_shared_eps<4>(cur + 16, eb);
+            if constexpr (GEN) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) { ea[i] = ga[i]; eb[i] = gb[i]; }
+                op[0] = make_float4(ea[0], ea[1], ea[2], ea[3]);
+                op[1] = make_float4(eb[0], eb[1], eb[2], eb[3]);
+                op += row / 4;
+                if (t + 1 < a.T)
+                    bm32_normals_x2<4>(philox4x32_10_dev(kg, (unsigned)(t + 1), a.step_lo, a.step_hi, a.keys),
+                                       philox4x32_10_dev(kg + 1u, (unsigned)(t + 1), a.step_lo, a.step_hi, a.keys),
+                                       ga, gb);
+            } else {
+                gp += row;
+                if (t + 1 < a.T) {
+                    cp_async_eps<4>(slot_sum - cur, gp);
+                    cp_async_eps<4>(slot_sum - cur + 16, gp + 4);
+                }
+                cp_async_commit();
+                cp_async_wait<1>();
+                load_shared_eps<4>(cur, ea);
+                load_shared_eps<4>(cur + 16, eb);
+            }
             const float4 u4 = rec->u, b4 = rec->b;
             const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
             const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
@@ -1040,6 +1091,19 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
                                     const float* U, const float* eps, float* costs_out) {
     RolloutArgs<typename Plant::Params> a;
     a.eps = eps;
+    a.eps_out = c.gen_eps;
+    a.cells = c.d_cells;
+    a.cent = c.d_cent;
+    a.cell_nx = c.cell_nx;
+    a.cell_ny = c.cell_ny;
+    a.n_cent = (int)c.cent_host.size();
+    a.cell_ox = c.cell_ox;
+    a.cell_oy = c.cell_oy;
+    a.cell_inv_h = c.cell_inv_h;
+    a.cell_band = c.cell_band;
+    a.step_lo = (unsigned)c.gen_step;
+    a.step_hi = (unsigned)(c.gen_step >> 32);
+    a.keys = philox_key_schedule(c.gen_seed);
     a.U = U;
     a.costs = c.d_costs;
     a.costs_out = costs_out;
@@ -1067,10 +1131,11 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
         a.obs_k[i] = i < c.n_obs_pairs ? c.obs_host[i] : make_float4(-1e15f, -1e15f, -1e15f, -1e15f);
     const int spt = X2 ? 2 : 1;                                      // samples per thread
     const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
-                        (size_t)2 * kRolloutThreads * spt * Plant::M * sizeof(float) +
-                        (DIAG ? 0 : (size_t)c.T * 2 * Plant::M * Plant::M * sizeof(float));
+                        (c.gen_eps ? 0 : (size_t)2 * kRolloutThreads * spt * Plant::M * sizeof(float)) +
+                        (DIAG ? 0 : (size_t)c.T * 2 * Plant::M * Plant::M * sizeof(float)) +
+                        (NP == kCellGrid ? c.cent_host.size() * sizeof(float2) + c.cells_host.size() * sizeof(uint32_t) : 0);
     const void* kern;
-    if constexpr (X2) kern = (const void*)rollout_kernel_x2<NP>;
+    if constexpr (X2) kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
     else kern = (const void*)rollout_kernel<Plant, DIAG, NP>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1087,6 +1152,10 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
 template <class Plant, bool DIAG, int NP>
 static cudaError_t dispatch_np(Ctx& c, const typename Plant::Params& P, const float* x0,
                                const float* U, const float* eps, float* costs_out) {
+    if constexpr (NP == 0) {
+        if (c.use_cells && c.cell_nx > 0 && c.pack2 && c.K_loc >= kPackedMinK)
+            return launch_rollout_t<Plant, DIAG, kCellGrid, true>(c, P, x0, U, eps, costs_out);
+    }
     if constexpr (NP > kMaxStaticPairs) {
         if (c.pack2 && c.K_loc >= kPackedMinK) return launch_rollout_t<Plant, DIAG, -1, true>(c, P, x0, U, eps, costs_out);
         return launch_rollout_t<Plant, DIAG, -1>(c, P, x0, U, eps, costs_out);
@@ -1112,6 +1181,11 @@ static cudaError_t launch_rollout_p(Ctx& c, const typename Plant::Params& P, con
                                     const float* U, const float* eps, float* costs_out) {
     return c.diag ? launch_rollout_np<Plant, true>(c, P, x0, U, eps, costs_out)
                   : launch_rollout_np<Plant, false>(c, P, x0, U, eps, costs_out);
+}
+
+bool fused_noise_applies(const Ctx& c) {
+    return c.fuse_noise && c.plant == MPPI_PLANT_QUADROTOR && c.diag && !c.per_t && c.pack2 &&
+           c.K_loc >= kPackedMinK;
 }
 
 cudaError_t launch_rollout(Ctx& c, const float* x0, const float* U, const float* eps,

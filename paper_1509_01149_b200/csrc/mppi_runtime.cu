@@ -4,6 +4,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -90,6 +91,96 @@ bool all_finite(const float* p, int n) {
     return true;
 }
 
+// Nearest-cylinder candidate grid for the packed quadrotor rollout (the obstacle term needs
+// min_j |p - c_j|^2).  Cells of side h tile the forest's bounding box plus a border;
+// a cell lists every centre j that no single other centre i beats over the whole cell:
+//   j is dropped iff some i has |p - c_i|^2 < |p - c_j|^2 - margin at all four corners of the cell
+//   grown by `slack` (the difference is affine in p, so the corners decide).
+// Every centre that can be the fp32 minimum for a point the kernel assigns to the cell is
+// therefore listed (slack >> the cell-assignment rounding, margin >> the fp32 error of d^2 over
+// the cell), and the minimum over the list equals the minimum over all centres bit for bit.
+// Border cells also cover a band of 100 spacings outside the grid (their rectangles are grown
+// outward; an affine difference still peaks at a corner).  Cells with more than kCellMaxCand
+// candidates, and points beyond the band, take the full loop.
+void build_cell_grid(Ctx& c, const float* xy, int n) {
+    c.cells_host.clear();
+    c.cent_host.clear();
+    c.cell_nx = c.cell_ny = 0;
+    if (n < 2 || n > (1 << kCellIdxBits)) return;
+    double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
+    for (int j = 0; j < n; ++j) {
+        xmin = fmin(xmin, xy[2 * j]); xmax = fmax(xmax, xy[2 * j]);
+        ymin = fmin(ymin, xy[2 * j + 1]); ymax = fmax(ymax, xy[2 * j + 1]);
+    }
+    std::vector<double> nn(n, 1e300);   // nearest-neighbour spacing sets the cell size
+    for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i)
+            if (i != j) nn[j] = fmin(nn[j], hypot((double)xy[2 * i] - xy[2 * j], (double)xy[2 * i + 1] - xy[2 * j + 1]));
+    std::vector<double> sorted = nn;
+    std::sort(sorted.begin(), sorted.end());
+    const double spacing = sorted[n / 2];
+    if (!(spacing > 1e-6) || !std::isfinite(xmax - xmin) || !std::isfinite(ymax - ymin)) return;
+    const double pad = 3.0 * spacing;
+    double h = 0.2 * spacing;
+    const double W = (xmax - xmin) + 2 * pad, H = (ymax - ymin) + 2 * pad;
+    const double kMaxCells = 8192.0;
+    if (W * H / (h * h) > kMaxCells) h = sqrt(W * H / kMaxCells);
+    const float inv_h = (float)(1.0 / h);
+    h = 1.0 / (double)inv_h;                                   // the cell size the kernel sees
+    const int nx = (int)ceil(W / h), ny = (int)ceil(H / h);
+    const double gx0 = (float)(xmin - pad), gy0 = (float)(ymin - pad);   // representable origin
+    // the kernel's fp32 cell assignment floor(fma(p, 1/h, -g0/h)) is off by < 1e-4 cells
+    const double band = ceil(100.0 * spacing / h);             // cells; beyond it: full search
+    const double slack = 1e-3 * h + 1e-6 * (fabs(gx0) + fabs(gy0) + W + H + 2 * band * h);
+    std::vector<uint32_t> words((size_t)nx * ny);
+    std::vector<double> d2(4 * (size_t)n);
+    std::vector<int> cand;
+    for (int iy = 0; iy < ny; ++iy)
+        for (int ix = 0; ix < nx; ++ix) {
+            // border cells also stand for the band of `band` cells outside the grid
+            const double x0 = gx0 + (ix == 0 ? -band : ix) * h - slack;
+            const double x1 = gx0 + (ix == nx - 1 ? nx + band : ix + 1) * h + slack;
+            const double y0 = gy0 + (iy == 0 ? -band : iy) * h - slack;
+            const double y1 = gy0 + (iy == ny - 1 ? ny + band : iy + 1) * h + slack;
+            const double px[4] = {x0, x0, x1, x1}, py[4] = {y0, y1, y0, y1};
+            for (int j = 0; j < n; ++j)
+                for (int k = 0; k < 4; ++k) {
+                    const double dx = px[k] - xy[2 * j], dy = py[k] - xy[2 * j + 1];
+                    d2[4 * j + k] = dx * dx + dy * dy;
+                }
+            cand.clear();
+            for (int j = 0; j < n; ++j) {
+                double mx = 0.0;
+                for (int k = 0; k < 4; ++k) mx = fmax(mx, d2[4 * j + k]);
+                const double margin = 1e-5 * mx + 1e-6;
+                bool dominated = false;
+                for (int i = 0; i < n && !dominated; ++i) {
+                    if (i == j) continue;
+                    bool all = true;
+                    for (int k = 0; k < 4 && all; ++k) all = d2[4 * i + k] < d2[4 * j + k] - margin;
+                    dominated = all;
+                }
+                if (!dominated) cand.push_back(j);
+            }
+            uint32_t w = 0;
+            if (!cand.empty() && (int)cand.size() <= kCellMaxCand) {
+                for (int s = 0; s < kCellMaxCand; ++s)
+                    w |= (uint32_t)cand[s < (int)cand.size() ? s : 0] << (kCellIdxBits * s);
+                w |= (uint32_t)cand.size() << 28;
+            }
+            words[(size_t)iy * nx + ix] = w;
+        }
+    c.cells_host.swap(words);
+    c.cent_host.resize(n);
+    for (int j = 0; j < n; ++j) c.cent_host[j] = make_float2(-xy[2 * j], -xy[2 * j + 1]);
+    c.cell_nx = nx;
+    c.cell_ny = ny;
+    c.cell_ox = (float)(-gx0 * (double)inv_h);
+    c.cell_oy = (float)(-gy0 * (double)inv_h);
+    c.cell_inv_h = inv_h;
+    c.cell_band = (float)band;
+}
+
 mppi_status_t digest_params(Ctx& c, const mppi_dynamics_t* d, const mppi_cost_t* q) {
     memset(&c.params, 0, sizeof(c.params));
     switch (c.plant) {
@@ -161,6 +252,7 @@ mppi_status_t digest_params(Ctx& c, const mppi_dynamics_t* d, const mppi_cost_t*
                 if (j % 2 == 0) { p.x = -Q.obstacles_xy[2 * j]; p.z = -Q.obstacles_xy[2 * j + 1]; }
                 else            { p.y = -Q.obstacles_xy[2 * j]; p.w = -Q.obstacles_xy[2 * j + 1]; }
             }
+            build_cell_grid(c, Q.obstacles_xy, n);
             return MPPI_OK;
         }
         case MPPI_PLANT_LINEAR: {
@@ -207,6 +299,8 @@ void free_ctx(Ctx& c) {
     c.ev_pending.clear();
     c.ev_pool.clear();
     cudaFree(c.d_obs);
+    cudaFree(c.d_cells);
+    cudaFree(c.d_cent);
     cudaFree(c.d_eps);
     cudaFree(c.d_costs);
     cudaFree(c.d_key_init);
@@ -257,14 +351,23 @@ mppi_status_t do_rollout(Ctx& c, const float* x0, const float* U, uint64_t seed,
     mppi_status_t s = sticky_check(c);
     if (s) return s;
     const float* eps = noise;
-    if (!noise) {
+    const bool fused = !noise && fused_noise_applies(c);
+    if (!noise && !fused) {
         MPPI_CUDA(launch_noise(c, seed, step, c.d_eps, true), "noise_kernel launch");
         eps = c.d_eps;
     } else {
         MPPI_CUDA(cudaMemcpyAsync(&c.d_stats->min_key, c.d_key_init, sizeof(long long),
                                   cudaMemcpyDeviceToDevice, c.stream), "min-key reset");
     }
-    MPPI_CUDA(launch_rollout(c, x0, U, eps, costs_out), "rollout_kernel launch");
+    if (fused) {   // the rollout draws eps itself and writes it to d_eps for the reduction
+        c.gen_eps = c.d_eps;
+        c.gen_seed = seed;
+        c.gen_step = step;
+        eps = c.d_eps;
+    }
+    const cudaError_t e = launch_rollout(c, x0, U, eps, costs_out);
+    c.gen_eps = nullptr;
+    MPPI_CUDA(e, "rollout_kernel launch");
     *eps_used = eps;
     return MPPI_OK;
 }
@@ -389,7 +492,10 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
         (a = dalloc(c, &c.d_eta_part, (size_t)c.n_chunks, "eta partials")) ||
         (a = dalloc(c, &c.d_stats, 1, "stats")) ||
         (a = dalloc(c, &c.d_U, (size_t)T * m, "U staging")) ||
-        (a = dalloc(c, &c.d_obs, (size_t)(c.n_obs_pairs > 0 ? c.n_obs_pairs : 1), "obstacles"))) {
+        (a = dalloc(c, &c.d_obs, (size_t)(c.n_obs_pairs > 0 ? c.n_obs_pairs : 1), "obstacles")) ||
+        (!c.cells_host.empty() &&
+         ((a = dalloc(c, &c.d_cells, c.cells_host.size(), "obstacle grid")) ||
+          (a = dalloc(c, &c.d_cent, c.cent_host.size(), "obstacle centres"))))) {
         free_ctx(c);
         delete ctx;
         return a;
@@ -404,7 +510,12 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
     if ((e = cudaMemcpy(c.d_key_init, &kinit, sizeof(kinit), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMemcpy(c.d_stats, &st0, sizeof(st0), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (c.n_obs_pairs > 0 &&
-         (e = cudaMemcpy(c.d_obs, c.obs_host.data(), c.n_obs_pairs * sizeof(float4), cudaMemcpyHostToDevice)) != cudaSuccess)) {
+         (e = cudaMemcpy(c.d_obs, c.obs_host.data(), c.n_obs_pairs * sizeof(float4), cudaMemcpyHostToDevice)) != cudaSuccess) ||
+        (!c.cells_host.empty() &&
+         ((e = cudaMemcpy(c.d_cells, c.cells_host.data(), c.cells_host.size() * sizeof(uint32_t),
+                          cudaMemcpyHostToDevice)) != cudaSuccess ||
+          (e = cudaMemcpy(c.d_cent, c.cent_host.data(), c.cent_host.size() * sizeof(float2),
+                          cudaMemcpyHostToDevice)) != cudaSuccess))) {
         free_ctx(c);
         delete ctx;
         return cuda_fail(e, "workspace init");
@@ -479,9 +590,16 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
     c.pending.clear();
     c.collect = true;
     const float* eps = noise ? noise : c.d_eps;
+    const bool fused = !noise && fused_noise_applies(c);
     cudaError_t e = cudaSuccess;
-    if (!noise) e = launch_noise(c, seed, step, c.d_eps, true);
+    if (!noise && !fused) e = launch_noise(c, seed, step, c.d_eps, true);
+    if (fused) {
+        c.gen_eps = c.d_eps;
+        c.gen_seed = seed;
+        c.gen_step = step;
+    }
     if (e == cudaSuccess) e = launch_rollout(c, x0, U, eps, nullptr);
+    c.gen_eps = nullptr;
     if (e == cudaSuccess) e = launch_reduce_update(c, eps, U);
     c.collect = false;
     if (e != cudaSuccess) return cuda_fail(e, "collecting the step's launches");
@@ -494,7 +612,7 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
         G = GraphState();
         MPPI_CUDA(cudaGraphCreate(&G.graph, 0), "cudaGraphCreate");
         cudaGraphNode_t prev = nullptr;
-        if (noise) {   // supplied noise: the min key is reset by a copy node instead of K1
+        if (noise || fused) {   // no K1 in the graph: the min key is reset by a copy node
             MPPI_CUDA(cudaGraphAddMemcpyNode1D(&prev, G.graph, nullptr, 0, &c.d_stats->min_key, c.d_key_init,
                                                sizeof(long long), cudaMemcpyDeviceToDevice), "memcpy node");
         }
@@ -530,6 +648,8 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
     switch (option) {
         case MPPI_OPTION_CUDA_GRAPH: ctx->c.use_graph = value != 0; return MPPI_OK;
         case MPPI_OPTION_PACKED_SAMPLES: ctx->c.pack2 = value != 0; return MPPI_OK;
+        case MPPI_OPTION_FUSED_NOISE: ctx->c.fuse_noise = value != 0; return MPPI_OK;
+        case MPPI_OPTION_OBSTACLE_GRID: ctx->c.use_cells = value != 0; return MPPI_OK;
         default: return fail(MPPI_ERR_INVALID_ARG, "unknown option %d", (int)option);
     }
 }

@@ -16,6 +16,10 @@ p.add_argument("--steps", type=int, default=2)
 a = p.parse_args()
 w = get(a.config)
 m = from_workload(w, K=a.K or w.K)
+from paper_1509_01149_b200 import _capi as A  # noqa: E402
+for kv in filter(None, os.environ.get("MPPI_OPTS", "").split(",")):   # e.g. OBSTACLE_GRID=0
+    k, v = kv.split("=")
+    m.set_option(getattr(A, "MPPI_OPTION_" + k), int(v))
 U = torch.tensor(w.U0, device="cuda")
 for i in range(a.steps):
     m.optimize(w.x0, U, w.seed, i)

@@ -402,6 +402,61 @@ def test_packed_two_sample_rollout_is_bitwise_scalar():
         assert torch.equal(Ua, Ub)
 
 
+@pytest.mark.parametrize("T", [200, 7])
+def test_fused_noise_rollout_is_bitwise_separate_pass(T):
+    """MPPI_OPTION_FUSED_NOISE: the packed rollout drawing its own noise gives the same costs, key
+    and update as the separate noise pass + rollout, and as the rollout fed K1's noise explicitly
+    (so the noise it draws, and writes for the reduction, is K1's bit for bit)."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get("C4", T=T)
+    for K in (1 << 16, (1 << 17) + 4):
+        a = from_workload(w, K=K)
+        b = from_workload(w, K=K)
+        b.set_option(A.MPPI_OPTION_FUSED_NOISE, 0)
+        U = cuda_u(w)
+        ca, ka = a.rollout_costs(w.x0, U, 11, 4)
+        cb, kb = b.rollout_costs(w.x0, U, 11, 4)
+        eps = b.noise(11, 4)
+        cc, kc = b.rollout_costs(w.x0, U, 11, 4, eps)
+        assert torch.equal(ca, cb) and torch.equal(ca, cc)
+        assert int(ka.item()) == int(kb.item()) == int(kc.item())
+        for graph in (True, False):
+            a.use_graph(graph)
+            Ua, Ub = U.clone(), U.clone()
+            for i in range(2):
+                a.optimize(w.x0, Ua, 11, i)
+                b.optimize(w.x0, Ub, 11, i)
+            assert torch.equal(Ua, Ub)
+        a.close()
+        b.close()
+
+
+@pytest.mark.parametrize("xy", [(0.0, 0.0), (25.0, 1.5), (44.0, -9.0), (300.0, 0.0), (-60.0, 80.0), (5000.0, 5.0)])
+def test_obstacle_grid_is_bitwise_full_search(xy):
+    """MPPI_OPTION_OBSTACLE_GRID: the per-cell candidate lists give the same nearest-cylinder
+    distance as the search over all 50 cylinders, hence identical costs, key and update; starts
+    outside the forest, inside it, at its edge and far outside the grid (full-search fallback)."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get("C4")
+    x0 = w.x0.copy()
+    x0[0], x0[1] = xy
+    x0[3] = 4.0                                     # flying along +x, so samples cross cells
+    a = from_workload(w, K=1 << 16)
+    b = from_workload(w, K=1 << 16)
+    b.set_option(A.MPPI_OPTION_OBSTACLE_GRID, 0)
+    U = cuda_u(w)
+    for seed in (1, 2):
+        ca, ka = a.rollout_costs(x0, U, seed, 0)
+        cb, kb = b.rollout_costs(x0, U, seed, 0)
+        assert torch.equal(ca, cb) and int(ka.item()) == int(kb.item())
+    Ua, Ub = cuda_u(w), cuda_u(w)
+    a.optimize(x0, Ua, 3, 0)
+    b.optimize(x0, Ub, 3, 0)
+    assert torch.equal(Ua, Ub)
+    a.close()
+    b.close()
+
+
 @pytest.mark.slow
 def test_closed_loop_c2_swings_up_like_the_oracle(oracle):
     """Alg. 1 receding horizon through the public API at C2 (K=4096, T=100,
