@@ -268,10 +268,14 @@ typedef enum {
                                           counters, bit-identical values, still written to the
                                           context's noise buffer for the reduction) instead of a
                                           separate noise pass (default 1) */
-    MPPI_OPTION_OBSTACLE_GRID = 4      /* packed quadrotor rollout: the nearest cylinder is searched
+    MPPI_OPTION_OBSTACLE_GRID = 4,     /* packed quadrotor rollout: the nearest cylinder is searched
                                           among a per-cell candidate list (host-built at create)
                                           instead of all cylinders; bitwise identical results
                                           (default 1) */
+    MPPI_OPTION_BULK_REDUCTION = 5     /* the weighted-noise reduction streams the noise through a
+                                          shared-memory ring filled by bulk copies (cp.async.bulk
+                                          + mbarrier) instead of per-thread loads; identical
+                                          results (default 1) */
 } mppi_option_t;
 
 /* mppi_set_option — execution options that never change results. */

@@ -17,6 +17,8 @@ namespace mppi {
 constexpr int kRolloutThreads = 128;
 constexpr int kWsumThreads = 256;
 constexpr int kWsumTT = 8;
+constexpr int kWsumStages = 3;                  // bulk-copy ring depth of wsum_tma_kernel
+constexpr size_t kWsumTmaSmem = (size_t)kWsumStages * kWsumTT * kWsumThreads * 16;   // 96 KB
 constexpr int kNoiseTT = 8;  // timesteps per noise thread
 constexpr int kMaxStaticPairs = 32;
 // the two-samples-per-thread quadrotor kernel is used from this many samples per GPU on (below
@@ -76,6 +78,7 @@ struct Ctx {
     double L64[16] = {0};           // chol(Sigma) fp64
     bool pack2 = true;              // quadrotor (diagonal): two samples per thread, FP32x2
     bool fuse_noise = true;         // packed rollout draws its own noise (no K1 pass)
+    bool tma_wsum = true;           // K3 streams eps with bulk copies (MPPI_OPTION_BULK_REDUCTION)
     // set around a fused launch: the rollout writes the noise it draws here (else nullptr)
     float* gen_eps = nullptr;
     uint64_t gen_seed = 0, gen_step = 0;

@@ -567,6 +567,160 @@ __global__ void __launch_bounds__(kWsumThreads) wsum_kernel(const WsumArgs a) {
     }
 }
 
+// K3 with the bulk-copy engine (sm_90+ cp.async.bulk, SASS UBLKCP): the same partial sums, but
+// the eps tiles stream into a kWsumStages-deep shared-memory ring filled by one thread with 1-D
+// bulk copies (one per timestep row, CW float4 columns) and mbarrier completion, so the bytes in
+// flight no longer depend on registers per thread.  Thread i owns column i of each CW-column
+// block of its chunk: the per-thread accumulation order over columns is the same as wsum_kernel.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+
+template <int M>
+__global__ void __launch_bounds__(kWsumThreads, 2) wsum_tma_kernel(const WsumArgs a) {
+    constexpr int SPC = 4 / M;
+    constexpr int TT = kWsumTT;
+    constexpr int CW = kWsumThreads;                 // float4 columns per block
+    constexpr int S = kWsumStages;
+    constexpr int NW = kWsumThreads / 32;
+    extern __shared__ __align__(128) float4 sbuf[];  // [S][TT][CW]
+    __shared__ __align__(8) uint64_t full[S], empty[S];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int chunk = blockIdx.x;
+    const int t0 = blockIdx.y * TT;
+    const int nt = min(TT, a.T - t0);
+    const float smin = key_cost(*a.key);
+    const long long c_begin = (long long)chunk * a.cols_per_chunk;
+    const long long c_end = min(a.ncols, c_begin + a.cols_per_chunk);
+    const long long nblk = c_end > c_begin ? (c_end - c_begin + CW - 1) / CW : 0;
+    const float4* __restrict__ eps4 = reinterpret_cast<const float4*>(a.eps);
+    const bool do_eta = blockIdx.y == 0;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](long long j) {
+        const int st = (int)(j % S);
+        const long long c0 = c_begin + j * CW;
+        const unsigned bytes = (unsigned)(min((long long)CW, c_end - c0) * sizeof(float4));
+        mbar_expect_tx(&full[st], bytes * nt);
+        for (int tt = 0; tt < nt; ++tt)
+            bulk_g2s(sbuf + ((size_t)st * TT + tt) * CW, eps4 + (size_t)(t0 + tt) * a.ncols + c0, bytes, &full[st]);
+    };
+    if (tid == 0)
+        for (long long j = 0; j < nblk && j < S; ++j) issue(j);
+    float acc[TT][4];
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[tt][c] = 0.0f;
+    float eta = 0.0f;
+    for (long long j = 0; j < nblk; ++j) {
+        const int st = (int)(j % S);
+        const unsigned parity = (unsigned)((j / S) & 1);
+        const long long col = c_begin + j * CW + tid;
+        const bool valid = col < c_end;
+        float w[SPC];
+        if (valid) {
+            float cs[SPC];
+            if constexpr (SPC == 4) {
+                const float4 c = __ldg(reinterpret_cast<const float4*>(a.costs) + col);
+                cs[0] = c.x; cs[1] = c.y; cs[2] = c.z; cs[3] = c.w;
+            } else if constexpr (SPC == 2) {
+                const float2 c = __ldg(reinterpret_cast<const float2*>(a.costs) + col);
+                cs[0] = c.x; cs[1] = c.y;
+            } else {
+                cs[0] = __ldg(a.costs + col);
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < SPC; ++s2) {
+                w[s2] = expf(-__fdiv_rn(cs[s2] - smin, a.lambda));   // PAPER.md:320 (min-shifted)
+                if (do_eta) eta += w[s2];
+            }
+        }
+        mbar_wait(&full[st], parity);
+        if (valid) {
+            const float4* tile = sbuf + (size_t)st * TT * CW + tid;
+#pragma unroll
+            for (int tt = 0; tt < TT; ++tt) {
+                if (tt < nt) {
+                    const float4 v = tile[tt * CW];
+                    acc[tt][0] = fmaf(w[0 / M], v.x, acc[tt][0]);
+                    acc[tt][1] = fmaf(w[1 / M], v.y, acc[tt][1]);
+                    acc[tt][2] = fmaf(w[2 / M], v.z, acc[tt][2]);
+                    acc[tt][3] = fmaf(w[3 / M], v.w, acc[tt][3]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (tid == 0 && j + S < nblk) {
+            mbar_wait(&empty[st], parity);   // every warp is done with block j: refill its slot
+            issue(j + S);
+        }
+    }
+    __shared__ float red[NW][TT * M + 1];
+    const int warp = tid >> 5;
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt) {
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+            float f = 0.0f;
+#pragma unroll
+            for (int s2 = 0; s2 < SPC; ++s2) f += acc[tt][s2 * M + jj];
+            f = warp_sum(f);
+            if (lane == 0) red[warp][tt * M + jj] = f;
+        }
+    }
+    eta = warp_sum(eta);
+    if (lane == 0) red[warp][TT * M] = eta;
+    __syncthreads();
+    if (tid < TT * M + 1) {
+        float sum = 0.0f;
+#pragma unroll
+        for (int w2 = 0; w2 < NW; ++w2) sum += red[w2][tid];
+        if (tid < TT * M) {
+            const int tt = tid / M, jj = tid % M;
+            if (tt < nt) a.part[((size_t)chunk * a.T + t0 + tt) * M + jj] = sum;
+        } else if (do_eta) {
+            a.eta_part[chunk] = sum;
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------ K4 finalize / apply
 struct FinalizeArgs {
     const float* part;
@@ -1223,6 +1377,15 @@ cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key) {
     a.cols_per_chunk = c.cols_per_chunk;
     a.lambda = c.lambda;
     const dim3 grid((unsigned)c.n_chunks, (unsigned)((c.T + kWsumTT - 1) / kWsumTT));
+    if (c.tma_wsum) {
+        const void* f = c.m == 1 ? (const void*)wsum_tma_kernel<1> : c.m == 2 ? (const void*)wsum_tma_kernel<2>
+                      : c.m == 4 ? (const void*)wsum_tma_kernel<4> : nullptr;
+        if (!f) return cudaErrorInvalidValue;
+        const size_t smem = kWsumTmaSmem;
+        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        return emit(c, f, grid, dim3(kWsumThreads), smem, &a, sizeof(a), MPPI_KERNEL_WSUM);
+    }
     const void* f = c.m == 1 ? (const void*)wsum_kernel<1> : c.m == 2 ? (const void*)wsum_kernel<2>
                   : c.m == 4 ? (const void*)wsum_kernel<4> : nullptr;
     if (!f) return cudaErrorInvalidValue;
@@ -1232,9 +1395,10 @@ cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key) {
 int wsum_blocks_per_sm(int m) {
     int n = 0;
     cudaError_t e = cudaErrorInvalidValue;
-    if (m == 1) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wsum_kernel<1>, kWsumThreads, 0);
-    if (m == 2) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wsum_kernel<2>, kWsumThreads, 0);
-    if (m == 4) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wsum_kernel<4>, kWsumThreads, 0);
+    const void* f = m == 1 ? (const void*)wsum_tma_kernel<1> : m == 2 ? (const void*)wsum_tma_kernel<2>
+                  : m == 4 ? (const void*)wsum_tma_kernel<4> : nullptr;
+    if (f && cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsumTmaSmem) == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, kWsumThreads, kWsumTmaSmem);
     return (e == cudaSuccess && n > 0) ? n : 1;
 }
 

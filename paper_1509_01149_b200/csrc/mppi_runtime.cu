@@ -650,6 +650,7 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
         case MPPI_OPTION_PACKED_SAMPLES: ctx->c.pack2 = value != 0; return MPPI_OK;
         case MPPI_OPTION_FUSED_NOISE: ctx->c.fuse_noise = value != 0; return MPPI_OK;
         case MPPI_OPTION_OBSTACLE_GRID: ctx->c.use_cells = value != 0; return MPPI_OK;
+        case MPPI_OPTION_BULK_REDUCTION: ctx->c.tma_wsum = value != 0; return MPPI_OK;
         default: return fail(MPPI_ERR_INVALID_ARG, "unknown option %d", (int)option);
     }
 }
