@@ -7,7 +7,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmppi_b200.so")
+# MPPI_LIB: an alternative in-tree build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("MPPI_LIB") or os.path.join(HERE, "libmppi_b200.so")
 
 MPPI_OK, MPPI_ERR_INVALID_ARG, MPPI_ERR_NOT_SPD, MPPI_ERR_OOM, MPPI_ERR_CUDA, MPPI_ERR_UNSUPPORTED = \
     0, 1, 2, 3, 4, 6

@@ -48,23 +48,29 @@ def up_to_date():
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
+def build(force=False, verbose=False, out=None, defines=()):
+    """Build the library (out/defines: an experimental variant, e.g. -DMPPI_X2_MINB=3)."""
+    lib = out or LIB
+    if not force and out is None and up_to_date():
         return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [NVCC] + ARCH + FLAGS + ["-I", os.path.join(ROOT, "include"), "-I", CSRC,
-                                   "-I", nccl_include(), "-shared", "-o", tmp] + sources() + ["-ldl"]
+    tmp = lib + ".tmp%d" % os.getpid()
+    cmd = [NVCC] + ARCH + FLAGS + list(defines) + ["-I", os.path.join(ROOT, "include"), "-I", CSRC,
+                                                   "-I", nccl_include(), "-shared", "-o", tmp] + sources() + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libmppi_b200.so")
-    with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
-        f.write(r.stderr)
+    if out is None:
+        with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
+            f.write(r.stderr)
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    defs = [a for a in args if a.startswith("-D")]
+    outs = [a[len("--out="):] for a in args if a.startswith("--out=")]
+    print(build(force=True, verbose="-v" in args, out=outs[0] if outs else None, defines=defs))

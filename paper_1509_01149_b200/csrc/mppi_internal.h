@@ -16,6 +16,9 @@ namespace mppi {
 
 constexpr int kRolloutThreads = 128;
 constexpr int kWsumThreads = 256;
+#ifndef MPPI_X2_MINB
+#define MPPI_X2_MINB 4
+#endif
 constexpr int kWsumTT = 8;
 constexpr int kWsumStages = 3;                  // bulk-copy ring depth of wsum_tma_kernel
 constexpr size_t kWsumTmaSmem = (size_t)kWsumStages * kWsumTT * kWsumThreads * 16;   // 96 KB

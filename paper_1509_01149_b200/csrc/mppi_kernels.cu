@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
 // use, and writes them to eps_out for K3; the noise pass and its HBM round trip disappear and the
 // integer/MUFU-heavy noise arithmetic fills issue slots the FMA-bound dynamics leaves idle.
 template <int NP, bool GEN>
-__global__ void __launch_bounds__(kRolloutThreads, 4)
+__global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
     rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
     constexpr int M = 4;
     extern __shared__ float4 smem4[];
@@ -403,6 +403,36 @@ __global__ void __launch_bounds__(kRolloutThreads, 4)
             cp_async_eps<4>(cur + 16, gp + 4);
             cp_async_commit();
         }
+        // one step t of both samples: v = U_t + s eps, IS_t, q(x_t), x <- x + F(x, v) dt, S~ += q~.
+        // SAFE: per-step accurate fallback; else the fast path, tracking max |angle| in amax.
+        float amax = 0.0f;
+        auto body = [&](auto SAFE, int t, const StepRec* rc, const float* ea, const float* eb) {
+            const float4 u4 = rc->u, b4 = rc->b;
+            const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+            V2 v[M];
+            V2 is = vb(rc->k.x);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const V2 e = vp(ea[i], eb[i]);
+                v[i] = fma2(vb(a.sd[i]), e, vb(uu[i]));                    // U_t + s_i eps_i
+                is = fma2(e, fma2(vb(a.ad[i]), e, vb(bb[i])), is);        // IS_t (PAPER.md:330)
+            }
+            const V2 q = st.template state_cost<NP>(t == 0, a.P, ob);    // q(x_t): step t-1
+            V2 xd[16];
+            if constexpr (decltype(SAFE)::value) {
+                if (st.deriv_fast(v, a.P, xd)) st.deriv_accurate(v, a.P, xd);
+            } else {
+                amax = fmaxf(amax, st.angle_absmax());
+                st.deriv_fast_unchecked(v, a.P, xd);
+            }
+            st.update(xd, a.dt);
+            S = S + (q + is);                                              // S~ += q~
+            if (a.qstep) {
+                if (t > 0) *reinterpret_cast<float2*>(a.qstep + (size_t)(t - 1) * a.K_loc + k) = (q + is_prev).v;
+                is_prev = is;
+            }
+        };
         const StepRec* rec = sRec;
         for (int t = 0; t < a.T; ++t, ++rec) {
             float ea[4], eb[4];
@@ -427,27 +457,25 @@ __global__ void __launch_bounds__(kRolloutThreads, 4)
                 load_shared_eps<4>(cur, ea);
                 load_shared_eps<4>(cur + 16, eb);
             }
-            const float4 u4 = rec->u, b4 = rec->b;
-            const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
-            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
-            V2 v[M];
-            V2 is = vb(rec->k.x);
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                const V2 e = vp(ea[i], eb[i]);
-                v[i] = fma2(vb(a.sd[i]), e, vb(uu[i]));                    // U_t + s_i eps_i
-                is = fma2(e, fma2(vb(a.ad[i]), e, vb(bb[i])), is);        // IS_t (PAPER.md:330)
-            }
-            const V2 q = st.template state_cost<NP>(t == 0, a.P, ob);    // q(x_t): step t-1
-            V2 xd[16];
-            if (st.deriv_fast(v, a.P, xd)) st.deriv_accurate(v, a.P, xd);
-            st.update(xd, a.dt);
-            S = S + (q + is);                                              // S~ += q~
-            if (a.qstep) {
-                if (t > 0) *reinterpret_cast<float2*>(a.qstep + (size_t)(t - 1) * a.K_loc + k) = (q + is_prev).v;
-                is_prev = is;
-            }
+            body(std::false_type(), t, rec, ea, eb);
             cur = slot_sum - cur;
+        }
+        if (__builtin_expect(!(amax <= kSinCosFastMax), 0)) {
+            // An angle left the fast sin/cos range somewhere on this pair's trajectories: replay
+            // both from x0 with the per-step accurate fallback (the inline-fallback semantics),
+            // reading back the noise this pass used.  Never taken on sane trajectories, and
+            // keeping the branch out of the hot loop lets the step body schedule as one block.
+            st.load(a.x0_dev ? a.x0_dev : a.x0);
+            S = vb(0.0f);
+            is_prev = vb(0.0f);
+            const float* ep = (GEN ? a.eps_out : a.eps) + (size_t)k * M;
+            rec = sRec;
+            for (int t = 0; t < a.T; ++t, ++rec, ep += row) {
+                const float4 e0 = *reinterpret_cast<const float4*>(ep);
+                const float4 e1 = *reinterpret_cast<const float4*>(ep + 4);
+                const float ea[4] = {e0.x, e0.y, e0.z, e0.w}, eb[4] = {e1.x, e1.y, e1.z, e1.w};
+                body(std::true_type(), t, rec, ea, eb);
+            }
         }
         const V2 qT = st.template state_cost<NP>(false, a.P, ob);         // q(x_T)
         S = S + qT;

@@ -402,6 +402,25 @@ def test_packed_two_sample_rollout_is_bitwise_scalar():
         assert torch.equal(Ua, Ub)
 
 
+@pytest.mark.parametrize("yaw,rate", [(1.2e5, 0.0), (105600.0, 60.0)])
+def test_packed_out_of_fast_range_replay_is_bitwise_scalar(yaw, rate):
+    """Yaw beyond the fast sin/cos range (all steps, or crossing it mid-horizon at different steps
+    per sample): the packed kernel's replay with the accurate fallback reproduces the scalar
+    kernel's per-step fallback bit for bit."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get("C4")
+    x0 = w.x0.copy()
+    x0[8], x0[11] = yaw, rate
+    a = from_workload(w, K=1 << 16)
+    b = from_workload(w, K=1 << 16)
+    b.set_option(A.MPPI_OPTION_PACKED_SAMPLES, 0)
+    U = cuda_u(w)
+    ca, ka = a.rollout_costs(x0, U, 7, 1)
+    cb, kb = b.rollout_costs(x0, U, 7, 1)
+    assert torch.isfinite(ca).all()
+    assert torch.equal(ca, cb) and int(ka.item()) == int(kb.item())
+
+
 @pytest.mark.parametrize("T", [200, 7])
 def test_fused_noise_rollout_is_bitwise_separate_pass(T):
     """MPPI_OPTION_FUSED_NOISE: the packed rollout drawing its own noise gives the same costs, key
