@@ -328,9 +328,9 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
 // Same per-step arithmetic and the same (cost, k) key as rollout_kernel.
 //
 // GEN: the kernel draws eps[t][k], eps[t][k+1] itself (Philox counters (k_global, t, step), the
-// same packed Box-Muller as K1, so the values are bit-identical to K1's) one step ahead of their
-// use, and writes them to eps_out for K3; the noise pass and its HBM round trip disappear and the
-// integer/MUFU-heavy noise arithmetic fills issue slots the FMA-bound dynamics leaves idle.
+// same packed Box-Muller as K1, so the values are bit-identical to K1's) in step t, and writes
+// them to eps_out for K3; the noise pass and its HBM round trip disappear and the integer/MUFU
+// noise arithmetic interleaves with the FMA-heavy dynamics of the same step.
 template <int NP, bool GEN>
 __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
     rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
@@ -394,11 +394,7 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
         unsigned cur = slot0;
         const unsigned kg = a.k_offset + (unsigned)k;
         float4* op = GEN ? reinterpret_cast<float4*>(a.eps_out + (size_t)k * M) : nullptr;
-        float ga[4], gb[4];                                             // GEN: eps of step t
-        if constexpr (GEN) {
-            bm32_normals_x2<4>(philox4x32_10_dev(kg, 0u, a.step_lo, a.step_hi, a.keys),
-                               philox4x32_10_dev(kg + 1u, 0u, a.step_lo, a.step_hi, a.keys), ga, gb);
-        } else {
+        if constexpr (!GEN) {
             cp_async_eps<4>(cur, gp);
             cp_async_eps<4>(cur + 16, gp + 4);
             cp_async_commit();
@@ -437,15 +433,13 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
         for (int t = 0; t < a.T; ++t, ++rec) {
             float ea[4], eb[4];
             if constexpr (GEN) {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) { ea[i] = ga[i]; eb[i] = gb[i]; }
+                // eps_t enters only the motor-lag derivative and IS_t, late in the step, so it is
+                // drawn in the same iteration and the scheduler overlaps it with the dynamics
+                bm32_normals_x2<4>(philox4x32_10_dev(kg, (unsigned)t, a.step_lo, a.step_hi, a.keys),
+                                   philox4x32_10_dev(kg + 1u, (unsigned)t, a.step_lo, a.step_hi, a.keys), ea, eb);
                 op[0] = make_float4(ea[0], ea[1], ea[2], ea[3]);
                 op[1] = make_float4(eb[0], eb[1], eb[2], eb[3]);
                 op += row / 4;
-                if (t + 1 < a.T)
-                    bm32_normals_x2<4>(philox4x32_10_dev(kg, (unsigned)(t + 1), a.step_lo, a.step_hi, a.keys),
-                                       philox4x32_10_dev(kg + 1u, (unsigned)(t + 1), a.step_lo, a.step_hi, a.keys),
-                                       ga, gb);
             } else {
                 gp += row;
                 if (t + 1 < a.T) {
