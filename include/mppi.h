@@ -263,8 +263,8 @@ typedef enum {
     MPPI_OPTION_PACKED_SAMPLES = 2,    /* quadrotor, diagonal Sigma and R, K_loc >= 65536: two samples
                                           per thread with FP32x2 arithmetic (default 1); bitwise
                                           identical results */
-    MPPI_OPTION_FUSED_NOISE = 3,       /* when the packed quadrotor rollout runs and the library draws
-                                          the noise: the rollout kernel draws it itself (same
+    MPPI_OPTION_FUSED_NOISE = 3,       /* when the library draws the noise, diagonal Sigma and R and
+                                          K_loc >= 65536: the rollout kernel draws it itself (same
                                           counters, bit-identical values, still written to the
                                           context's noise buffer for the reduction) instead of a
                                           separate noise pass (default 1) */

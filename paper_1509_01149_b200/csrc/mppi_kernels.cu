@@ -187,7 +187,10 @@ struct RolloutArgs {
 // the same polynomial in eps with the per-t constants staged in shared memory.
 // eps[t][k] reaches the thread through a kEpsStages-deep shared-memory ring filled by per-thread
 // cp.async two steps ahead, so the HBM latency is hidden without tying up registers.
-template <class Plant, bool DIAG, int NP>
+//
+// GEN (diagonal Sigma and R, plants other than the quadrotor, whose large-K path is the packed
+// kernel): eps[t][k] is drawn in step t with K1's counters and transform and written to eps_out.
+template <class Plant, bool DIAG, int NP, bool GEN = false>
 __global__ void __launch_bounds__(kRolloutThreads, 8)
     rollout_kernel(const __grid_constant__ RolloutArgs<typename Plant::Params> a) {
     constexpr int M = Plant::M;
@@ -285,23 +288,34 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
                 is_prev = is;
             }
         };
-        // eps ring: two slots, the copy for step t+1 is issued before step t is computed
-        const float* gp = a.eps + (size_t)k * M;
-        const unsigned slot0 = (unsigned)__cvta_generic_to_shared(sRing + tid * M);
-        const unsigned slot_sum = 2u * slot0 + blockDim.x * M * (unsigned)sizeof(float);
-        unsigned cur = slot0;                                          // other slot = slot_sum - cur
-        cp_async_eps<M>(cur, gp);
-        cp_async_commit();
         const StepRec* rec = sRec;
-        for (int t = 0; t < a.T; ++t, ++rec) {
-            gp += row;
-            if (t + 1 < a.T) cp_async_eps<M>(slot_sum - cur, gp);      // step t+1 in flight
+        if constexpr (GEN) {
+            const unsigned kg = a.k_offset + (unsigned)k;
+            float* op = a.eps_out + (size_t)k * M;
+            for (int t = 0; t < a.T; ++t, ++rec, op += row) {
+                float e[M];
+                bm32_normals<M>(philox4x32_10_dev(kg, (unsigned)t, a.step_lo, a.step_hi, a.keys), e);
+                store_eps<M>(op, e);
+                one_step(rec, e, t == 0, t);
+            }
+        } else {
+            // eps ring: two slots, the copy for step t+1 is issued before step t is computed
+            const float* gp = a.eps + (size_t)k * M;
+            const unsigned slot0 = (unsigned)__cvta_generic_to_shared(sRing + tid * M);
+            const unsigned slot_sum = 2u * slot0 + blockDim.x * M * (unsigned)sizeof(float);
+            unsigned cur = slot0;                                      // other slot = slot_sum - cur
+            cp_async_eps<M>(cur, gp);
             cp_async_commit();
-            cp_async_wait<1>();                                        // step t has landed
-            float e[M];
-            load_shared_eps<M>(cur, e);
-            one_step(rec, e, t == 0, t);
-            cur = slot_sum - cur;
+            for (int t = 0; t < a.T; ++t, ++rec) {
+                gp += row;
+                if (t + 1 < a.T) cp_async_eps<M>(slot_sum - cur, gp);  // step t+1 in flight
+                cp_async_commit();
+                cp_async_wait<1>();                                    // step t has landed
+                float e[M];
+                load_shared_eps<M>(cur, e);
+                one_step(rec, e, t == 0, t);
+                cur = slot_sum - cur;
+            }
         }
         const float qT = st.template state_cost<NP>(false, a.P, ob);  // q(x_T), step T-1
         S += qT;
@@ -1311,8 +1325,14 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
                         (DIAG ? 0 : (size_t)c.T * 2 * Plant::M * Plant::M * sizeof(float)) +
                         (NP == kCellGrid ? c.cent_host.size() * sizeof(float2) + c.cells_host.size() * sizeof(uint32_t) : 0);
     const void* kern;
-    if constexpr (X2) kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
-    else kern = (const void*)rollout_kernel<Plant, DIAG, NP>;
+    if constexpr (X2) {
+        kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
+    } else if constexpr (DIAG && !std::is_same<Plant, Quadrotor>::value) {
+        kern = c.gen_eps ? (const void*)rollout_kernel<Plant, DIAG, NP, true> : (const void*)rollout_kernel<Plant, DIAG, NP>;
+    } else {
+        if (c.gen_eps) return cudaErrorInvalidValue;   // fused_noise_applies() excludes this variant
+        kern = (const void*)rollout_kernel<Plant, DIAG, NP>;
+    }
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -1360,8 +1380,11 @@ static cudaError_t launch_rollout_p(Ctx& c, const typename Plant::Params& P, con
 }
 
 bool fused_noise_applies(const Ctx& c) {
-    return c.fuse_noise && c.plant == MPPI_PLANT_QUADROTOR && c.diag && !c.per_t && c.pack2 &&
-           c.K_loc >= kPackedMinK;
+    if (!c.fuse_noise || !c.diag || c.per_t) return false;
+    if (c.plant == MPPI_PLANT_QUADROTOR) return c.pack2 && c.K_loc >= kPackedMinK;   // packed kernel
+    // one-sample GEN kernel: only once the step is throughput-bound (measured: -2..4 % at
+    // K = 2^20; at small K the per-thread noise lengthens the latency-bound step loop)
+    return c.K_loc >= kPackedMinK;
 }
 
 cudaError_t launch_rollout(Ctx& c, const float* x0, const float* U, const float* eps,

@@ -9,6 +9,8 @@ from mppi_inputs import get  # noqa: E402
 from paper_1509_01149_b200 import _capi as A, from_workload  # noqa: E402
 
 w = get(os.environ.get("CFG", "C5"))
+if os.environ.get("K"):
+    w.K = int(os.environ["K"])
 for spec in sys.argv[1:]:
     m = from_workload(w)
     for kv in spec.split(","):

@@ -421,14 +421,16 @@ def test_packed_out_of_fast_range_replay_is_bitwise_scalar(yaw, rate):
     assert torch.equal(ca, cb) and int(ka.item()) == int(kb.item())
 
 
-@pytest.mark.parametrize("T", [200, 7])
-def test_fused_noise_rollout_is_bitwise_separate_pass(T):
-    """MPPI_OPTION_FUSED_NOISE: the packed rollout drawing its own noise gives the same costs, key
-    and update as the separate noise pass + rollout, and as the rollout fed K1's noise explicitly
-    (so the noise it draws, and writes for the reduction, is K1's bit for bit)."""
+@pytest.mark.parametrize("cfg,T,Ks", [("C4", 200, (1 << 16, (1 << 17) + 4)), ("C4", 7, (1 << 16,)),
+                                       ("C1", 50, (1 << 16, 65540)), ("C3", 20, (1 << 16, 65540))])
+def test_fused_noise_rollout_is_bitwise_separate_pass(cfg, T, Ks):
+    """MPPI_OPTION_FUSED_NOISE: the rollout drawing its own noise (packed quadrotor kernel, and the
+    one-sample kernel for the other plants) gives the same costs, key and update as the separate
+    noise pass + rollout, and as the rollout fed K1's noise explicitly (so the noise it draws, and
+    writes for the reduction, is K1's bit for bit)."""
     from paper_1509_01149_b200 import _capi as A
-    w = get("C4", T=T)
-    for K in (1 << 16, (1 << 17) + 4):
+    w = get(cfg, T=T)
+    for K in Ks:
         a = from_workload(w, K=K)
         b = from_workload(w, K=K)
         b.set_option(A.MPPI_OPTION_FUSED_NOISE, 0)
