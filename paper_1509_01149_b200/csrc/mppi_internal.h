@@ -20,7 +20,10 @@ constexpr int kWsumThreads = 256;
 #define MPPI_X2_MINB 4
 #endif
 constexpr int kWsumTT = 8;
-constexpr int kWsumStages = 3;                  // bulk-copy ring depth of wsum_tma_kernel
+constexpr int kWsumStages = 3;
+constexpr int kEpsStages = 4;                   // one-sample rollout's cp.async ring depth
+constexpr int64_t kSmallMaxK = 16384;           // single-launch step up to this K_loc
+constexpr size_t kSmallEpsSmemMax = 160 * 1024; // its eps tile goes to shared memory below this                  // bulk-copy ring depth of wsum_tma_kernel
 constexpr size_t kWsumTmaSmem = (size_t)kWsumStages * kWsumTT * kWsumThreads * 16;   // 96 KB
 constexpr int kNoiseTT = 8;  // timesteps per noise thread
 constexpr int kMaxStaticPairs = 32;

@@ -178,28 +178,117 @@ struct RolloutArgs {
     PhiloxKeys keys;
 };
 
-// One sample per thread.  Per step t (PAPER.md:358-363):
-//   v = U_t + du,  du = sqrt(nu) L eps[t][k]                 (PAPER.md:308, :312, :361)
-//   x <- x + F(x, v) dt,  S~ += q(x) + IS_t                    (PAPER.md:362)
-//   IS_t = (1 - 1/nu)/2 du'R du + U_t'R du + U_t'R U_t/2       (PAPER.md:329-331)
-// With diagonal L and R (every shipped config) IS_t is evaluated as
-//   IS_t = K_t + sum_i e_i (a_i e_i + b_ti),  b_ti = s_i (R U_t)_i,  K_t = U_t'R U_t/2,
-// the same polynomial in eps with the per-t constants staged in shared memory.
-// eps[t][k] reaches the thread through a kEpsStages-deep shared-memory ring filled by per-thread
-// cp.async two steps ahead, so the HBM latency is hidden without tying up registers.
-//
-// GEN (diagonal Sigma and R, plants other than the quadrotor, whose large-K path is the packed
-// kernel): eps[t][k] is drawn in step t with K1's counters and transform and written to eps_out.
-template <class Plant, bool DIAG, int NP, bool GEN = false>
-__global__ void __launch_bounds__(kRolloutThreads, 8)
-    rollout_kernel(const __grid_constant__ RolloutArgs<typename Plant::Params> a) {
-    constexpr int M = Plant::M;
-    extern __shared__ float4 smem4[];
-    float4* sObs = smem4;
-    StepRec* sRec = reinterpret_cast<StepRec*>(smem4 + a.n_obs_pairs);   // per-t constants [T]
-    float* sRing = reinterpret_cast<float*>(sRec + a.T);               // eps ring [2][blockDim][M]
-    // general path: per-t sampling factor F_t and IS matrix G_t after the ring ([T][2][M*M])
-    float* sMat = sRing + 2 * blockDim.x * M;
+// Per-thread stream of eps[t][k] (M floats) for t = 0..T-1 through a kEpsStages-slot shared
+// memory ring (sRing: [kEpsStages][blockDim][M]) filled by cp.async: the copy for step
+// t + kEpsStages - 1 is issued before step t is consumed, so at small K (a step shorter than an
+// L2 round trip) the step loop does not wait on memory.  f(t, e) consumes step t.
+template <int M, class F>
+__device__ __forceinline__ void eps_ring_loop(const float* eps, size_t row, int T, int k, float* sRing, F&& f) {
+    constexpr int S = kEpsStages;
+    const unsigned slot0 = (unsigned)__cvta_generic_to_shared(sRing + threadIdx.x * M);
+    const unsigned slot_stride = blockDim.x * M * (unsigned)sizeof(float);
+    const float* gp = eps + (size_t)k * M;                             // next step to issue
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j) {
+        if (j < T) cp_async_eps<M>(slot0 + j * slot_stride, gp + j * row);
+        cp_async_commit();
+    }
+    gp += (size_t)(S - 1) * row;
+    int slot_issue = S - 1, slot_use = 0;
+    for (int t = 0; t < T; ++t) {
+        if (t + S - 1 < T) cp_async_eps<M>(slot0 + slot_issue * slot_stride, gp);
+        cp_async_commit();
+        gp += row;
+        slot_issue = slot_issue + 1 == S ? 0 : slot_issue + 1;
+        cp_async_wait<S - 1>();                                        // step t has landed
+        float e[M];
+        load_shared_eps<M>(slot0 + slot_use * slot_stride, e);
+        slot_use = slot_use + 1 == S ? 0 : slot_use + 1;
+        f(t, e);
+    }
+}
+
+// One sample's rollout state and its step t for the one-sample kernels.
+// sMat: per-t F_t, G_t of the general path (!DIAG).
+template <class Plant, bool DIAG, int NP>
+struct ScalarRollout {
+    static constexpr int M = Plant::M;
+    const RolloutArgs<typename Plant::Params>& a;
+    const ObstacleView& ob;
+    const float* sMat;
+    int k;
+    Plant st;
+    float S = 0.0f;
+    float is_prev = 0.0f;                                              // IS term of step t-1
+
+    __device__ __forceinline__ ScalarRollout(const RolloutArgs<typename Plant::Params>& a_, const ObstacleView& ob_,
+                                             const float* sMat_, int k_)
+        : a(a_), ob(ob_), sMat(sMat_), k(k_) {
+        st.load(a.x0_dev ? a.x0_dev : a.x0, 0);
+    }
+
+    __device__ __forceinline__ void step(const StepRec* rec, const float* e, bool first, int t) {
+        const float4 u4 = rec->u;
+        const float4 b4 = rec->b;
+        const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+        const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+        float v[M];
+        float is = rec->k.x;
+        if (DIAG) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                v[i] = fmaf(a.sd[i], e[i], uu[i]);                     // U_t + s_i eps_i
+                is = fmaf(e[i], fmaf(a.ad[i], e[i], bb[i]), is);       // IS_t
+            }
+        } else {
+            // du = F_t eps (F_t = A_t L, NEXT-3; default sqrt(nu) L), IS_t = du'G_t du + (R U_t).du + K_t
+            const float* F = sMat + t * 2 * M * M;
+            const float* G = F + M * M;
+            float du[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                float d = 0.0f;
+#pragma unroll
+                for (int j = 0; j < M; ++j) d = fmaf(F[i * M + j], e[j], d);
+                du[i] = d;
+                v[i] = uu[i] + d;
+            }
+            float duGdu = 0.0f, uRdu = 0.0f;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+#pragma unroll
+                for (int j = 0; j < M; ++j) duGdu = fmaf(du[i] * G[i * M + j], du[j], duGdu);
+                uRdu = fmaf(bb[i], du[i], uRdu);
+            }
+            is = duGdu + (uRdu + is);
+        }
+        // rotated step: q(x_t) (the cost of step t-1, 0 at t = 0) and F(x_t, v_t) only need
+        // x_t, so they share one basic block; then x_{t+1} = x_t + F dt
+        const float q = st.template state_cost<NP>(first, a.P, ob);
+        float xd[Plant::N];
+        if (st.deriv_fast(v, a.P, xd)) st.deriv_accurate(v, a.P, xd);   // |angle| > 105615: rare
+        st.update(xd, a.dt);
+        S += q + is;                                                   // S~ += q~
+        if (a.qstep) {                                                 // q~_{t-1} = q(x_t) + IS_{t-1}
+            if (!first) a.qstep[(size_t)(t - 1) * a.K_loc + k] = q + is_prev;
+            is_prev = is;
+        }
+    }
+
+    // + q(x_T) (the cost of step T-1); non-finite -> penalty
+    __device__ __forceinline__ float finish() {
+        const float qT = st.template state_cost<NP>(false, a.P, ob);
+        S += qT;
+        if (a.qstep) a.qstep[(size_t)(a.T - 1) * a.K_loc + k] = qT + is_prev;
+        if (!isfinite(S)) S = a.penalty;
+        return S;
+    }
+};
+
+// Stage the per-t constants U_t, s_i (R U_t)_i, U_t'R U_t / 2 (and, !DIAG, F_t, G_t), the
+// obstacle pairs and (NP == kCellGrid) nothing else: callers add their own tables.
+template <int M, bool DIAG, class PP>
+__device__ __forceinline__ void stage_step_constants(const RolloutArgs<PP>& a, float4* sObs, StepRec* sRec, float* sMat) {
     const int tid = threadIdx.x;
     for (int i = tid; i < a.n_obs_pairs; i += blockDim.x) sObs[i] = a.obs[i];
     if (!DIAG) {
@@ -228,66 +317,42 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
         r.k = make_float4(0.5f * kk, 0.0f, 0.0f, 0.0f);
         sRec[t] = r;
     }
+}
+
+// One sample per thread.  Per step t (PAPER.md:358-363):
+//   v = U_t + du,  du = sqrt(nu) L eps[t][k]                 (PAPER.md:308, :312, :361)
+//   x <- x + F(x, v) dt,  S~ += q(x) + IS_t                    (PAPER.md:362)
+//   IS_t = (1 - 1/nu)/2 du'R du + U_t'R du + U_t'R U_t/2       (PAPER.md:329-331)
+// With diagonal L and R (every shipped config) IS_t is evaluated as
+//   IS_t = K_t + sum_i e_i (a_i e_i + b_ti),  b_ti = s_i (R U_t)_i,  K_t = U_t'R U_t/2,
+// the same polynomial in eps with the per-t constants staged in shared memory.
+// eps[t][k] reaches the thread through a kEpsStages-deep shared-memory ring filled by per-thread
+// cp.async two steps ahead, so the HBM latency is hidden without tying up registers.
+//
+// GEN (diagonal Sigma and R, plants other than the quadrotor, whose large-K path is the packed
+// kernel): eps[t][k] is drawn in step t with K1's counters and transform and written to eps_out.
+template <class Plant, bool DIAG, int NP, bool GEN = false>
+__global__ void __launch_bounds__(kRolloutThreads, 8)
+    rollout_kernel(const __grid_constant__ RolloutArgs<typename Plant::Params> a) {
+    constexpr int M = Plant::M;
+    extern __shared__ float4 smem4[];
+    float4* sObs = smem4;
+    StepRec* sRec = reinterpret_cast<StepRec*>(smem4 + a.n_obs_pairs);   // per-t constants [T]
+    float* sRing = reinterpret_cast<float*>(sRec + a.T);               // eps ring [kEpsStages][blockDim][M]
+    // general path: per-t sampling factor F_t and IS matrix G_t after the ring ([T][2][M*M])
+    float* sMat = sRing + kEpsStages * blockDim.x * M;
+    const int tid = threadIdx.x;
+    stage_step_constants<M, DIAG>(a, sObs, sRec, sMat);
     __syncthreads();
 
     const int k = blockIdx.x * blockDim.x + tid;
     long long key = LLONG_MAX;
     if (k < a.K_loc) {
-        Plant st;
-        st.load(a.x0_dev ? a.x0_dev : a.x0, 0);
         // compile-time pair count: read the forest from the kernel-parameter constant bank
         // (uniform-register operands, no per-thread registers); else shared memory
         const ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
+        ScalarRollout<Plant, DIAG, NP> ro(a, ob, sMat, k);
         const size_t row = (size_t)a.K_loc * M;
-        float S = 0.0f;
-        float is_prev = 0.0f;                                          // IS term of step t-1
-        auto one_step = [&](const StepRec* rec, const float* e, bool first, int t) {
-            const float4 u4 = rec->u;
-            const float4 b4 = rec->b;
-            const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
-            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
-            float v[M];
-            float is = rec->k.x;
-            if (DIAG) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    v[i] = fmaf(a.sd[i], e[i], uu[i]);                 // U_t + s_i eps_i
-                    is = fmaf(e[i], fmaf(a.ad[i], e[i], bb[i]), is);   // IS_t
-                }
-            } else {
-                // du = F_t eps (F_t = A_t L, NEXT-3; default sqrt(nu) L), IS_t = du'G_t du + (R U_t).du + K_t
-                const float* F = sMat + t * 2 * M * M;
-                const float* G = F + M * M;
-                float du[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    float d = 0.0f;
-#pragma unroll
-                    for (int j = 0; j < M; ++j) d = fmaf(F[i * M + j], e[j], d);
-                    du[i] = d;
-                    v[i] = uu[i] + d;
-                }
-                float duGdu = 0.0f, uRdu = 0.0f;
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-#pragma unroll
-                    for (int j = 0; j < M; ++j) duGdu = fmaf(du[i] * G[i * M + j], du[j], duGdu);
-                    uRdu = fmaf(bb[i], du[i], uRdu);
-                }
-                is = duGdu + (uRdu + is);
-            }
-            // rotated step: q(x_t) (the cost of step t-1, 0 at t = 0) and F(x_t, v_t) only need
-            // x_t, so they share one basic block; then x_{t+1} = x_t + F dt
-            const float q = st.template state_cost<NP>(first, a.P, ob);
-            float xd[Plant::N];
-            if (st.deriv_fast(v, a.P, xd)) st.deriv_accurate(v, a.P, xd);   // |angle| > 105615: rare
-            st.update(xd, a.dt);
-            S += q + is;                                               // S~ += q~
-            if (a.qstep) {                                             // q~_{t-1} = q(x_t) + IS_{t-1}
-                if (!first) a.qstep[(size_t)(t - 1) * a.K_loc + k] = q + is_prev;
-                is_prev = is;
-            }
-        };
         const StepRec* rec = sRec;
         if constexpr (GEN) {
             const unsigned kg = a.k_offset + (unsigned)k;
@@ -296,31 +361,12 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
                 float e[M];
                 bm32_normals<M>(philox4x32_10_dev(kg, (unsigned)t, a.step_lo, a.step_hi, a.keys), e);
                 store_eps<M>(op, e);
-                one_step(rec, e, t == 0, t);
+                ro.step(rec, e, t == 0, t);
             }
         } else {
-            // eps ring: two slots, the copy for step t+1 is issued before step t is computed
-            const float* gp = a.eps + (size_t)k * M;
-            const unsigned slot0 = (unsigned)__cvta_generic_to_shared(sRing + tid * M);
-            const unsigned slot_sum = 2u * slot0 + blockDim.x * M * (unsigned)sizeof(float);
-            unsigned cur = slot0;                                      // other slot = slot_sum - cur
-            cp_async_eps<M>(cur, gp);
-            cp_async_commit();
-            for (int t = 0; t < a.T; ++t, ++rec) {
-                gp += row;
-                if (t + 1 < a.T) cp_async_eps<M>(slot_sum - cur, gp);  // step t+1 in flight
-                cp_async_commit();
-                cp_async_wait<1>();                                    // step t has landed
-                float e[M];
-                load_shared_eps<M>(cur, e);
-                one_step(rec, e, t == 0, t);
-                cur = slot_sum - cur;
-            }
+            eps_ring_loop<M>(a.eps, row, a.T, k, sRing, [&](int t, const float* e) { ro.step(rec++, e, t == 0, t); });
         }
-        const float qT = st.template state_cost<NP>(false, a.P, ob);  // q(x_T), step T-1
-        S += qT;
-        if (a.qstep) a.qstep[(size_t)(a.T - 1) * a.K_loc + k] = qT + is_prev;
-        if (!isfinite(S)) S = a.penalty;                               // SURVEY A15
+        const float S = ro.finish();
         a.costs[k] = S;
         if (a.costs_out) a.costs_out[k] = S;
         key = cost_key(S, a.k_offset + (unsigned)k);
@@ -1276,10 +1322,10 @@ cudaError_t launch_noise(Ctx& c, uint64_t seed, uint64_t step, float* out, bool 
     return emit(c, f, grid, dim3(256), 0, &a, sizeof(a), MPPI_KERNEL_NOISE);
 }
 
-template <class Plant, bool DIAG, int NP, bool X2 = false>
-static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, const float* x0,
-                                    const float* U, const float* eps, float* costs_out) {
-    RolloutArgs<typename Plant::Params> a;
+// The rollout kernels' argument block from the context (eps: the noise read by non-GEN kernels).
+template <class Plant>
+static void fill_rollout_args(Ctx& c, const typename Plant::Params& P, const float* x0, const float* U,
+                              const float* eps, float* costs_out, RolloutArgs<typename Plant::Params>& a) {
     a.eps = eps;
     a.eps_out = c.gen_eps;
     a.cells = c.d_cells;
@@ -1319,9 +1365,16 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     a.P = P;
     for (int i = 0; i < kMaxStaticPairs; ++i)
         a.obs_k[i] = i < c.n_obs_pairs ? c.obs_host[i] : make_float4(-1e15f, -1e15f, -1e15f, -1e15f);
+}
+
+template <class Plant, bool DIAG, int NP, bool X2 = false>
+static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, const float* x0,
+                                    const float* U, const float* eps, float* costs_out) {
+    RolloutArgs<typename Plant::Params> a;
+    fill_rollout_args<Plant>(c, P, x0, U, eps, costs_out, a);
     const int spt = X2 ? 2 : 1;                                      // samples per thread
     const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
-                        (c.gen_eps ? 0 : (size_t)2 * kRolloutThreads * spt * Plant::M * sizeof(float)) +
+                        (c.gen_eps ? 0 : (size_t)(X2 ? 2 : kEpsStages) * kRolloutThreads * spt * Plant::M * sizeof(float)) +
                         (DIAG ? 0 : (size_t)c.T * 2 * Plant::M * Plant::M * sizeof(float)) +
                         (NP == kCellGrid ? c.cent_host.size() * sizeof(float2) + c.cells_host.size() * sizeof(uint32_t) : 0);
     const void* kern;
