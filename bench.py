@@ -370,7 +370,15 @@ def main():
     # CPU-side check of the same sharded path): the split-phase calls + torch.distributed
     lib_nccl = world > 1 and args.backend == "nccl"
     if lib_nccl:
-        m.attach_nccl()
+        ok = 1
+        try:
+            m.attach_nccl()
+        except Exception as e:      # still a GPU path: the split phase + torch.distributed NCCL
+            print("bench.py: mppi_nccl_attach failed (%s); using ShardedMPPI" % e, file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], device="cuda", dtype=torch.int32)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)     # every rank takes the same path
+        lib_nccl = bool(flag.item())
     sh = ShardedMPPI(m) if world > 1 and not lib_nccl else None
 
     def step(i, Ut):
