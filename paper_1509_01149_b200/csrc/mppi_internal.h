@@ -21,7 +21,10 @@ constexpr int kWsumThreads = 256;
 #endif
 constexpr int kWsumTT = 8;
 constexpr int kWsumStages = 3;
-constexpr int kEpsStages = 4;                   // one-sample rollout's cp.async ring depth
+constexpr int kEpsStages = 4;
+constexpr int kWsumCtgStages = 2;               // wsum_ctg_tma_kernel ring depth (eps + cost-to-go tiles)
+// eps float4 + (4/m) cost-to-go floats per column: 80 KB (m = 4) .. 128 KB (m = 1)
+constexpr size_t wsum_ctg_tma_smem(int m) { return (size_t)kWsumCtgStages * kWsumTT * kWsumThreads * (16 + 16 / m); }                   // one-sample rollout's cp.async ring depth
 constexpr int64_t kSmallMaxK = 16384;           // single-launch step up to this K_loc
 constexpr size_t kSmallEpsSmemMax = 160 * 1024; // its eps tile goes to shared memory below this                  // bulk-copy ring depth of wsum_tma_kernel
 constexpr size_t kWsumTmaSmem = (size_t)kWsumStages * kWsumTT * kWsumThreads * 16;   // 96 KB

@@ -870,17 +870,26 @@ __global__ void __launch_bounds__(256) ctg_kernel(const CtgArgs a) {
     const int k = blockIdx.x * 256 + threadIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float s = 0.0f;
-    for (int t = a.T - 1; t >= 0; --t) {
-        float v = INFINITY;
-        if (k < a.K_loc) {
-            float* p = a.ctg + (size_t)t * a.K_loc + k;
-            s += *p;
-            v = isfinite(s) ? s : a.penalty;
-            *p = v;
-        }
+    constexpr int B = 8;                 // rows loaded ahead: the suffix sum is a serial chain
+    for (int t1 = a.T - 1; t1 >= 0; t1 -= B) {
+        float q[B];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (lane == 0) wmin_t[warp * a.T + t] = v;
+        for (int i = 0; i < B; ++i)
+            q[i] = (k < a.K_loc && t1 - i >= 0) ? a.ctg[(size_t)(t1 - i) * a.K_loc + k] : 0.0f;
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            const int t = t1 - i;
+            if (t < 0) break;
+            float v = INFINITY;
+            if (k < a.K_loc) {
+                s += q[i];
+                v = isfinite(s) ? s : a.penalty;
+                a.ctg[(size_t)t * a.K_loc + k] = v;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+            if (lane == 0) wmin_t[warp * a.T + t] = v;
+        }
     }
     __syncthreads();
     for (int t = threadIdx.x; t < a.T; t += 256) {
@@ -924,7 +933,7 @@ struct WsumCtgArgs {
     float* eta_part;      // [n_chunks][T]
     int T, K_loc;
     long long ncols, cols_per_chunk;
-    float lambda;
+    float neg_inv_lambda;   // -1/lambda (fp32 of the fp64 value)
 };
 
 template <int M>
@@ -954,7 +963,9 @@ __global__ void __launch_bounds__(kWsumThreads) wsum_ctg_kernel(const WsumCtgArg
                 float w[SPC];
 #pragma unroll
                 for (int s = 0; s < SPC; ++s) {
-                    w[s] = expf(-__fdiv_rn(crow[s] - sm, a.lambda));
+                    // exp(-(S - S_min,t)/lambda) with a precomputed -1/lambda: no division slow
+                    // path in the unrolled t-tile, so all its loads issue before the arithmetic
+                    w[s] = expf(__fmul_rn(crow[s] - sm, a.neg_inv_lambda));
                     eta[tt] += w[s];
                 }
                 const float4 v = __ldcs(eps4 + (size_t)t * a.ncols + col);
@@ -991,6 +1002,120 @@ __global__ void __launch_bounds__(kWsumThreads) wsum_ctg_kernel(const WsumCtgArg
         } else {
             const int tt = threadIdx.x - TT * M;
             if (tt < nt) a.eta_part[(size_t)chunk * a.T + t0 + tt] = s;
+        }
+    }
+}
+
+// wsum_ctg_kernel with the bulk-copy engine: each stage holds TT rows of CW float4 eps columns
+// and the matching TT x (CW * SPC) cost-to-go values; same per-thread accumulation order.
+template <int M>
+__global__ void __launch_bounds__(kWsumThreads, 2) wsum_ctg_tma_kernel(const WsumCtgArgs a) {
+    constexpr int SPC = 4 / M;
+    constexpr int TT = kWsumTT;
+    constexpr int CW = kWsumThreads;
+    constexpr int S = kWsumCtgStages;
+    constexpr int NW = kWsumThreads / 32;
+    extern __shared__ __align__(128) float4 sbuf[];   // [S][TT][CW] eps, then [S][TT][CW*SPC] ctg
+    float* sctg = reinterpret_cast<float*>(sbuf + (size_t)S * TT * CW);
+    __shared__ __align__(8) uint64_t full[S], empty[S];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int chunk = blockIdx.x;
+    const int t0 = blockIdx.y * TT;
+    const int nt = min(TT, a.T - t0);
+    const long long c_begin = (long long)chunk * a.cols_per_chunk;
+    const long long c_end = min(a.ncols, c_begin + a.cols_per_chunk);
+    const long long nblk = c_end > c_begin ? (c_end - c_begin + CW - 1) / CW : 0;
+    const float4* __restrict__ eps4 = reinterpret_cast<const float4*>(a.eps);
+    if (tid == 0) {
+        for (int s2 = 0; s2 < S; ++s2) {
+            mbar_init(&full[s2], 1);
+            mbar_init(&empty[s2], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](long long j) {
+        const int st = (int)(j % S);
+        const long long c0 = c_begin + j * CW;
+        const long long cols = min((long long)CW, c_end - c0);
+        const unsigned eb = (unsigned)(cols * sizeof(float4));
+        const unsigned cb = (unsigned)(cols * SPC * sizeof(float));
+        mbar_expect_tx(&full[st], (eb + cb) * nt);
+        for (int tt = 0; tt < nt; ++tt) {
+            bulk_g2s(sbuf + ((size_t)st * TT + tt) * CW, eps4 + (size_t)(t0 + tt) * a.ncols + c0, eb, &full[st]);
+            bulk_g2s(sctg + ((size_t)st * TT + tt) * CW * SPC, a.ctg + (size_t)(t0 + tt) * a.K_loc + c0 * SPC, cb, &full[st]);
+        }
+    };
+    if (tid == 0)
+        for (long long j = 0; j < nblk && j < S; ++j) issue(j);
+    float acc[TT][4], eta[TT];
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt) {
+        eta[tt] = 0.0f;
+#pragma unroll
+        for (int c2 = 0; c2 < 4; ++c2) acc[tt][c2] = 0.0f;
+    }
+    float sm[TT];
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt) sm[tt] = tt < nt ? a.smin[t0 + tt] : 0.0f;
+    for (long long j = 0; j < nblk; ++j) {
+        const int st = (int)(j % S);
+        const unsigned parity = (unsigned)((j / S) & 1);
+        const bool valid = c_begin + j * CW + tid < c_end;
+        mbar_wait(&full[st], parity);
+        if (valid) {
+            const float4* tile = sbuf + (size_t)st * TT * CW + tid;
+            const float* ctile = sctg + (size_t)st * TT * CW * SPC + tid * SPC;
+#pragma unroll
+            for (int tt = 0; tt < TT; ++tt) {
+                if (tt < nt) {
+                    float w[SPC];
+#pragma unroll
+                    for (int s2 = 0; s2 < SPC; ++s2) {
+                        w[s2] = expf(__fmul_rn(ctile[tt * CW * SPC + s2] - sm[tt], a.neg_inv_lambda));
+                        eta[tt] += w[s2];
+                    }
+                    const float4 v = tile[tt * CW];
+                    acc[tt][0] = fmaf(w[0 / M], v.x, acc[tt][0]);
+                    acc[tt][1] = fmaf(w[1 / M], v.y, acc[tt][1]);
+                    acc[tt][2] = fmaf(w[2 / M], v.z, acc[tt][2]);
+                    acc[tt][3] = fmaf(w[3 / M], v.w, acc[tt][3]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (tid == 0 && j + S < nblk) {
+            mbar_wait(&empty[st], parity);
+            issue(j + S);
+        }
+    }
+    __shared__ float red[NW][TT * (M + 1)];
+    const int warp = tid >> 5;
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt) {
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+            float f = 0.0f;
+#pragma unroll
+            for (int s2 = 0; s2 < SPC; ++s2) f += acc[tt][s2 * M + jj];
+            f = warp_sum(f);
+            if (lane == 0) red[warp][tt * M + jj] = f;
+        }
+        const float e = warp_sum(eta[tt]);
+        if (lane == 0) red[warp][TT * M + tt] = e;
+    }
+    __syncthreads();
+    if (tid < TT * (M + 1)) {
+        float sum = 0.0f;
+#pragma unroll
+        for (int w2 = 0; w2 < NW; ++w2) sum += red[w2][tid];
+        if (tid < TT * M) {
+            const int tt = tid / M, jj = tid % M;
+            if (tt < nt) a.part[((size_t)chunk * a.T + t0 + tt) * M + jj] = sum;
+        } else {
+            const int tt = tid - TT * M;
+            if (tt < nt) a.eta_part[(size_t)chunk * a.T + t0 + tt] = sum;
         }
     }
 }
@@ -1057,8 +1182,17 @@ cudaError_t launch_wsum_ctg(Ctx& c, const float* eps) {
     a.K_loc = (int)c.K_loc;
     a.ncols = c.K_loc * c.m / 4;
     a.cols_per_chunk = c.cols_per_chunk;
-    a.lambda = c.lambda;
+    a.neg_inv_lambda = (float)(-1.0 / (double)c.lambda);
     const dim3 grid((unsigned)c.n_chunks, (unsigned)((c.T + kWsumTT - 1) / kWsumTT));
+    if (c.tma_wsum) {
+        const void* f = c.m == 1 ? (const void*)wsum_ctg_tma_kernel<1> : c.m == 2 ? (const void*)wsum_ctg_tma_kernel<2>
+                      : c.m == 4 ? (const void*)wsum_ctg_tma_kernel<4> : nullptr;
+        if (!f) return cudaErrorInvalidValue;
+        const size_t smem = wsum_ctg_tma_smem(c.m);
+        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        return emit(c, f, grid, dim3(kWsumThreads), smem, &a, sizeof(a), MPPI_KERNEL_WSUM);
+    }
     const void* f = c.m == 1 ? (const void*)wsum_ctg_kernel<1> : c.m == 2 ? (const void*)wsum_ctg_kernel<2>
                   : c.m == 4 ? (const void*)wsum_ctg_kernel<4> : nullptr;
     if (!f) return cudaErrorInvalidValue;

@@ -482,6 +482,8 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
     if (nch > max_ch) nch = max_ch;
     if (nch < 1) nch = 1;
     c.cols_per_chunk = (ncols + nch - 1) / nch;
+    // whole 256-column blocks: every bulk copy of the reduction kernels starts 16-B aligned
+    c.cols_per_chunk = (c.cols_per_chunk + kWsumThreads - 1) / kWsumThreads * kWsumThreads;
     c.n_chunks = (int)((ncols + c.cols_per_chunk - 1) / c.cols_per_chunk);
 
     mppi_status_t a;

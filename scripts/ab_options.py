@@ -13,7 +13,9 @@ if os.environ.get("K"):
     w.K = int(os.environ["K"])
 for spec in sys.argv[1:]:
     m = from_workload(w)
-    for kv in spec.split(","):
+    if os.environ.get("CTG"):
+        m.set_weighting(True)
+    for kv in filter(None, spec.split(",")):
         k, v = kv.split("=")
         m.set_option(getattr(A, "MPPI_OPTION_" + k), int(v))
     U = torch.tensor(w.U0, device="cuda")

@@ -17,6 +17,8 @@ a = p.parse_args()
 w = get(a.config)
 m = from_workload(w, K=a.K or w.K)
 from paper_1509_01149_b200 import _capi as A  # noqa: E402
+if os.environ.get("CTG"):
+    m.set_weighting(True)
 for kv in filter(None, os.environ.get("MPPI_OPTS", "").split(",")):   # e.g. OBSTACLE_GRID=0
     k, v = kv.split("=")
     m.set_option(getattr(A, "MPPI_OPTION_" + k), int(v))
