@@ -19,15 +19,16 @@ constexpr int kWsumThreads = 256;
 #ifndef MPPI_X2_MINB
 #define MPPI_X2_MINB 4
 #endif
-constexpr int kWsumTT = 8;
-constexpr int kWsumStages = 3;
-constexpr int kEpsStages = 4;
+constexpr int kWsumTT = 8;                      // timestep rows per reduction CTA
+#ifndef MPPI_WSUM_STAGES
+#define MPPI_WSUM_STAGES 2
+#endif
+constexpr int kWsumStages = MPPI_WSUM_STAGES;   // bulk-copy ring depth of wsum_tma_kernel
+constexpr size_t kWsumTmaSmem = (size_t)kWsumStages * kWsumTT * kWsumThreads * 16;   // 64 KB: 3 CTAs / SM
 constexpr int kWsumCtgStages = 2;               // wsum_ctg_tma_kernel ring depth (eps + cost-to-go tiles)
 // eps float4 + (4/m) cost-to-go floats per column: 80 KB (m = 4) .. 128 KB (m = 1)
-constexpr size_t wsum_ctg_tma_smem(int m) { return (size_t)kWsumCtgStages * kWsumTT * kWsumThreads * (16 + 16 / m); }                   // one-sample rollout's cp.async ring depth
-constexpr int64_t kSmallMaxK = 16384;           // single-launch step up to this K_loc
-constexpr size_t kSmallEpsSmemMax = 160 * 1024; // its eps tile goes to shared memory below this                  // bulk-copy ring depth of wsum_tma_kernel
-constexpr size_t kWsumTmaSmem = (size_t)kWsumStages * kWsumTT * kWsumThreads * 16;   // 96 KB
+constexpr size_t wsum_ctg_tma_smem(int m) { return (size_t)kWsumCtgStages * kWsumTT * kWsumThreads * (16 + 16 / m); }
+constexpr int kEpsStages = 4;                   // one-sample rollout's cp.async ring depth
 constexpr int kNoiseTT = 8;  // timesteps per noise thread
 constexpr int kMaxStaticPairs = 32;
 // the two-samples-per-thread quadrotor kernel is used from this many samples per GPU on (below

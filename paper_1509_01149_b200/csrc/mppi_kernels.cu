@@ -688,7 +688,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 
 template <int M>
-__global__ void __launch_bounds__(kWsumThreads, 2) wsum_tma_kernel(const WsumArgs a) {
+__global__ void __launch_bounds__(kWsumThreads, 3) wsum_tma_kernel(const WsumArgs a) {
     constexpr int SPC = 4 / M;
     constexpr int TT = kWsumTT;
     constexpr int CW = kWsumThreads;                 // float4 columns per block
