@@ -89,6 +89,7 @@ struct Ctx {
     bool pack2 = true;              // quadrotor (diagonal): two samples per thread, FP32x2
     bool fuse_noise = true;         // packed rollout draws its own noise (no K1 pass)
     bool tma_wsum = true;           // K3 streams eps with bulk copies (MPPI_OPTION_BULK_REDUCTION)
+    bool use_pdl = false;           // programmatic kernel->kernel edges in the step graph (MPPI_OPTION_PDL)
     // set around a fused launch: the rollout writes the noise it draws here (else nullptr)
     float* gen_eps = nullptr;
     uint64_t gen_seed = 0, gen_step = 0;

@@ -45,6 +45,13 @@ __device__ __forceinline__ void store_eps(float* p, const float* z) {
     }
 }
 
+// Programmatic dependent launch (MPPI_OPTION_PDL: the step graph's kernel->kernel edges are
+// programmatic): a kernel's CTAs may be launched as its predecessor's last CTAs exit; pdl_wait()
+// blocks until the predecessor grid has completed and its memory is visible (a no-op for an
+// ordinary launch).  No kernel triggers its successor early: measured on B200, early triggers
+// let waiting reduction CTAs crowd the rollout (C2 42 -> 118 us).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // Per-thread asynchronous copy of one noise element group (4m bytes) into shared memory
 // (LDGSTS: cp.async, non-blocking, no register tied to the load).  dst: shared-window address.
 template <int M>
@@ -344,6 +351,7 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
     const int tid = threadIdx.x;
     stage_step_constants<M, DIAG>(a, sObs, sRec, sMat);
     __syncthreads();
+    pdl_wait();                        // eps and the min-key reset of the noise pass
 
     const int k = blockIdx.x * blockDim.x + tid;
     long long key = LLONG_MAX;
@@ -428,6 +436,7 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
         sRec[t] = r;
     }
     __syncthreads();
+    pdl_wait();
 
     const int k = 2 * (blockIdx.x * blockDim.x + tid);                 // samples k, k+1
     long long key = LLONG_MAX;
@@ -572,6 +581,7 @@ struct WsumArgs {
 // 16-byte loads in flight per iteration.  w_k is computed once per sample per t-tile.
 template <int M>
 __global__ void __launch_bounds__(kWsumThreads) wsum_kernel(const WsumArgs a) {
+    pdl_wait();
     constexpr int SPC = 4 / M;  // samples per float4 column
     constexpr int TT = kWsumTT;
     const int chunk = blockIdx.x;
@@ -700,7 +710,6 @@ __global__ void __launch_bounds__(kWsumThreads, 3) wsum_tma_kernel(const WsumArg
     const int chunk = blockIdx.x;
     const int t0 = blockIdx.y * TT;
     const int nt = min(TT, a.T - t0);
-    const float smin = key_cost(*a.key);
     const long long c_begin = (long long)chunk * a.cols_per_chunk;
     const long long c_end = min(a.ncols, c_begin + a.cols_per_chunk);
     const long long nblk = c_end > c_begin ? (c_end - c_begin + CW - 1) / CW : 0;
@@ -714,6 +723,8 @@ __global__ void __launch_bounds__(kWsumThreads, 3) wsum_tma_kernel(const WsumArg
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    pdl_wait();                        // costs, key and eps of the rollout
+    const float smin = key_cost(*a.key);
     auto issue = [&](long long j) {
         const int st = (int)(j % S);
         const long long c0 = c_begin + j * CW;
@@ -818,6 +829,7 @@ struct FinalizeArgs {
 };
 
 __global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeArgs a) {
+    pdl_wait();
     extern __shared__ float sA[];  // [1 + T*M]: eta, A
     const int TM = a.T * a.M;
     if (a.buf_in) {

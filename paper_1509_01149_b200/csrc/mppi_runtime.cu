@@ -618,14 +618,26 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
             MPPI_CUDA(cudaGraphAddMemcpyNode1D(&prev, G.graph, nullptr, 0, &c.d_stats->min_key, c.d_key_init,
                                                sizeof(long long), cudaMemcpyDeviceToDevice), "memcpy node");
         }
+        bool prev_is_kernel = false;
         for (KLaunch& L : c.pending) {
             cudaKernelNodeParams p = node_params(L);
             cudaGraphNode_t node;
-            MPPI_CUDA(cudaGraphAddKernelNode(&node, G.graph, prev ? &prev : nullptr, prev ? 1 : 0, &p),
-                      "cudaGraphAddKernelNode");
+            MPPI_CUDA(cudaGraphAddKernelNode(&node, G.graph, nullptr, 0, &p), "cudaGraphAddKernelNode");
+            if (prev) {
+                // kernel -> kernel: programmatic edge (the successor starts while the predecessor
+                // drains and waits in griddepcontrol.wait before touching its outputs)
+                cudaGraphEdgeData ed;
+                memset(&ed, 0, sizeof(ed));
+                if (prev_is_kernel && c.use_pdl) {
+                    ed.from_port = cudaGraphKernelNodePortProgrammatic;
+                    ed.type = cudaGraphDependencyTypeProgrammatic;
+                }
+                MPPI_CUDA(cudaGraphAddDependencies_v2(G.graph, &prev, &node, &ed, 1), "graph edge");
+            }
             G.nodes.push_back(node);
             G.funcs.push_back(L.func);
             prev = node;
+            prev_is_kernel = true;
         }
         MPPI_CUDA(cudaGraphInstantiate(&G.exec, G.graph, 0), "cudaGraphInstantiate");
     } else {
@@ -653,6 +665,11 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
         case MPPI_OPTION_FUSED_NOISE: ctx->c.fuse_noise = value != 0; return MPPI_OK;
         case MPPI_OPTION_OBSTACLE_GRID: ctx->c.use_cells = value != 0; return MPPI_OK;
         case MPPI_OPTION_BULK_REDUCTION: ctx->c.tma_wsum = value != 0; return MPPI_OK;
+        case MPPI_OPTION_PDL:
+            MPPI_CUDA(cudaStreamSynchronize(ctx->c.stream), "stream sync");
+            ctx->c.use_pdl = value != 0;
+            free_graphs(ctx->c);   // the edges are baked into the graph
+            return MPPI_OK;
         default: return fail(MPPI_ERR_INVALID_ARG, "unknown option %d", (int)option);
     }
 }
