@@ -452,6 +452,24 @@ def test_fused_noise_rollout_is_bitwise_separate_pass(cfg, T, Ks):
         b.close()
 
 
+@pytest.mark.parametrize("cfg,K", [("C2", 4096), ("C3", 16384), ("C4", 65536)])
+def test_pdl_graph_is_bitwise_plain_graph(cfg, K):
+    """MPPI_OPTION_PDL: programmatic kernel->kernel edges change launch timing only."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get(cfg)
+    a = from_workload(w, K=K)
+    b = from_workload(w, K=K)
+    a.set_option(A.MPPI_OPTION_PDL, 1)
+    Ua, Ub = cuda_u(w), cuda_u(w)
+    for i in range(3):
+        a.optimize(w.x0, Ua, 4, i)
+        b.optimize(w.x0, Ub, 4, i)
+    torch.cuda.synchronize()
+    assert torch.equal(Ua, Ub) and a.stats() == b.stats()
+    a.close()
+    b.close()
+
+
 @pytest.mark.parametrize("xy", [(0.0, 0.0), (25.0, 1.5), (44.0, -9.0), (300.0, 0.0), (-60.0, 80.0), (5000.0, 5.0)])
 def test_obstacle_grid_is_bitwise_full_search(xy):
     """MPPI_OPTION_OBSTACLE_GRID: the per-cell candidate lists give the same nearest-cylinder
