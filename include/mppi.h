@@ -309,7 +309,8 @@ mppi_status_t mppi_nccl_unique_id(uint8_t* id);
  *   (8 B) -> local weights and weighted noise sums -> ncclAllReduce(SUM) of [eta, A] ((1+T m) fp32)
  *   -> the same U update on every rank (U stays a bit-identical replica).
  * A single-rank communicator (world == 1) is allowed (the collectives are identities).
- * The cost-to-go weighting is not supported with a communicator in this version. */
+ * With MPPI_WEIGHTS_COST_TO_GO the collectives are MIN over the T per-step minima of the
+ * cost-to-go and SUM over [eta_t (T), A (T m)] instead. */
 mppi_status_t mppi_nccl_attach(mppi_ctx* ctx, const uint8_t* id);
 
 /* ---------------------------------------------------------------- split phase (multi-GPU) */
@@ -363,7 +364,9 @@ typedef enum {
 
 /* mppi_set_weighting — selects the estimator of the update (synchronises the stream).  The
  * cost-to-go mode allocates a [T][K_loc] fp32 buffer of per-step costs on first use, adds 8 B
- * of HBM traffic per sample-step and a per-(t,k) exp; world == 1 only (else UNSUPPORTED). */
+ * of HBM traffic per sample-step and a per-(t,k) exp.  Sharded (world > 1) it runs through
+ * mppi_nccl_attach + mppi_optimize: allreduce MIN over the T per-step minima, then SUM over
+ * [eta_t (T), A (T m)]; the split-phase calls refuse it (UNSUPPORTED). */
 mppi_status_t mppi_set_weighting(mppi_ctx* ctx, mppi_weighting_t mode);
 
 /* mppi_cost_to_go — copies S~_{t,k} of the last cost-to-go step into `out` (DEVICE float

@@ -144,7 +144,7 @@ struct Ctx {
     GraphState graphs[2];
     // row (e): a communicator the library drives itself (mppi_nccl_attach)
     void* nccl = nullptr;                 // ncclComm_t
-    float* d_commbuf = nullptr;           // [1 + T*m]: [eta, A] all-reduced across ranks
+    float* d_commbuf = nullptr;           // [T + T*m]: [eta, A] (trajectory: 1 + T*m used) all-reduced across ranks
 };
 
 // Launch (or collect, see Ctx::collect) one kernel whose single parameter is `args`.
@@ -176,11 +176,13 @@ int nccl_attach(Ctx& c, const unsigned char* id_bytes);
 void nccl_detach(Ctx& c);
 const char* nccl_error(int r);
 int nccl_min_key(Ctx& c, long long* key);
+int nccl_min_f32(Ctx& c, float* buf, size_t count);
 int nccl_sum_buf(Ctx& c, float* buf, size_t count);
 cudaError_t launch_fk_reduce(Ctx& c, double* part, int nblk);   // Feynman-Kac partial sums
 cudaError_t launch_ctg(Ctx& c);                                  // cost-to-go + per-t minima
 cudaError_t launch_wsum_ctg(Ctx& c, const float* eps);
-cudaError_t launch_finalize_ctg(Ctx& c, float* U);
+// buf_out: write [eta_t, A] (partials for the SUM allreduce); buf_in: apply from the summed buffer
+cudaError_t launch_finalize_ctg(Ctx& c, float* U, const float* buf_in = nullptr, float* buf_out = nullptr);
 cudaError_t launch_advance(Ctx& c, float* x, float* U, const float* u_init, float* x_log,
                            float* u_log, float* q_log);             // closed-loop plant step + shift
 

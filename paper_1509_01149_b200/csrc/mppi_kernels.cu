@@ -1137,6 +1137,8 @@ struct FinalizeCtgArgs {
     const float* part;
     const float* eta_part;
     int n_chunks;
+    const float* buf_in;   // [T + T*M] = [eta_t, A] already summed over ranks, or nullptr
+    float* buf_out;        // [T + T*M] (partials mode: no update), or nullptr
     float* U;
     DeviceStats* stats;
     int T, M;
@@ -1144,17 +1146,36 @@ struct FinalizeCtgArgs {
     const float* mats;
 };
 
+// fixed-order sums over chunks, then U_t += sqrt(nu) L A_t / eta_t.  Sharded (row e): a
+// partials pass writes [eta_t, A] for the SUM allreduce, an apply pass reads it back; the
+// arithmetic is the same as the one-pass form, so one rank reproduces it bit for bit.
 __global__ void __launch_bounds__(1024) finalize_ctg_kernel(const FinalizeCtgArgs a) {
+    pdl_wait();
     const int TM = a.T * a.M;
+    if (a.buf_out) {
+        for (int o = threadIdx.x; o < a.T + TM; o += blockDim.x) {
+            float v = 0.0f;
+            if (o < a.T) {
+                for (int c = 0; c < a.n_chunks; ++c) v += a.eta_part[(size_t)c * a.T + o];
+            } else {
+                const int tj = o - a.T, t = tj / a.M, j = tj % a.M;
+                for (int c = 0; c < a.n_chunks; ++c) v += a.part[((size_t)c * a.T + t) * a.M + j];
+            }
+            a.buf_out[o] = v;
+        }
+        return;
+    }
     for (int o = threadIdx.x; o < TM; o += blockDim.x) {
         const int t = o / a.M, i = o % a.M;
         float eta = 0.0f;
-        for (int c = 0; c < a.n_chunks; ++c) eta += a.eta_part[(size_t)c * a.T + t];
+        if (a.buf_in) eta = a.buf_in[t];
+        else for (int c = 0; c < a.n_chunks; ++c) eta += a.eta_part[(size_t)c * a.T + t];
         float d = 0.0f;
         const int jmax = a.mats ? a.M - 1 : i;
         for (int j = 0; j <= jmax; ++j) {
             float A = 0.0f;
-            for (int c = 0; c < a.n_chunks; ++c) A += a.part[((size_t)c * a.T + t) * a.M + j];
+            if (a.buf_in) A = a.buf_in[a.T + t * a.M + j];
+            else for (int c = 0; c < a.n_chunks; ++c) A += a.part[((size_t)c * a.T + t) * a.M + j];
             const float f = a.mats ? a.mats[t * 32 + i * a.M + j] : a.sL[i * a.M + j];
             d = __fadd_rn(d, __fmul_rn(f, A));
         }
@@ -1211,18 +1232,21 @@ cudaError_t launch_wsum_ctg(Ctx& c, const float* eps) {
     return emit(c, f, grid, dim3(kWsumThreads), 0, &a, sizeof(a), MPPI_KERNEL_WSUM);
 }
 
-cudaError_t launch_finalize_ctg(Ctx& c, float* U) {
+cudaError_t launch_finalize_ctg(Ctx& c, float* U, const float* buf_in, float* buf_out) {
     FinalizeCtgArgs a;
     a.part = c.d_part;
     a.eta_part = c.d_ctg_eta;
     a.n_chunks = c.n_chunks;
+    a.buf_in = buf_in;
+    a.buf_out = buf_out;
     a.U = U;
     a.stats = c.d_stats;
     a.T = c.T;
     a.M = c.m;
     for (int i = 0; i < 16; ++i) a.sL[i] = c.sL[i];
     a.mats = c.per_t ? c.d_mats : nullptr;
-    const int threads = c.T * c.m >= 1024 ? 1024 : ((c.T * c.m + 31) / 32) * 32;
+    const int n = c.T * c.m + (buf_out ? c.T : 0);
+    const int threads = n >= 1024 ? 1024 : ((n + 31) / 32) * 32;
     return emit(c, (const void*)finalize_ctg_kernel, dim3(1), dim3(threads), 0, &a, sizeof(a),
                 MPPI_KERNEL_FINALIZE);
 }

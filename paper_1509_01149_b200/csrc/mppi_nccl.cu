@@ -79,6 +79,11 @@ int nccl_min_key(Ctx& c, long long* key) {
     return (int)api().all_reduce(key, key, 1, ncclInt64, ncclMin, (ncclComm_t)c.nccl, c.stream);
 }
 
+// element-wise minimum of fp32 values over ranks, in place (per-t cost-to-go minima)
+int nccl_min_f32(Ctx& c, float* buf, size_t count) {
+    return (int)api().all_reduce(buf, buf, count, ncclFloat32, ncclMin, (ncclComm_t)c.nccl, c.stream);
+}
+
 // sum of [eta, A[0..T*m)] over ranks, in place
 int nccl_sum_buf(Ctx& c, float* buf, size_t count) {
     return (int)api().all_reduce(buf, buf, count, ncclFloat32, ncclSum, (ncclComm_t)c.nccl, c.stream);

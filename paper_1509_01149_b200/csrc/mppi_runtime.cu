@@ -679,12 +679,25 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
 // on every rank.  All on the context stream; direct launches.
 static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t seed, uint64_t step,
                                    const float* noise) {
-    if (c.ctg) return fail(MPPI_ERR_UNSUPPORTED, "cost-to-go weighting with a communicator (round 1: world 1)");
     c.last_launches = 0;
     const float* eps = nullptr;
     if (mppi_status_t s = do_rollout(c, x0, U, seed, step, noise, nullptr, &eps)) return s;
     int r = nccl_min_key(c, &c.d_stats->min_key);
     if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(MIN key): %s", nccl_error(r));
+    if (c.ctg) {
+        // NEXT-1 sharded: local suffix sums and per-t minima -> MIN over the T
+        // minima -> per-(t, k) weights and local sums -> SUM of [eta_t (T), A (T m)] -> update
+        MPPI_CUDA(launch_ctg(c), "cost-to-go launch");
+        r = nccl_min_f32(c, c.d_ctg_smin, (size_t)c.T);
+        if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(MIN S_t): %s", nccl_error(r));
+        MPPI_CUDA(launch_wsum_ctg(c, eps), "wsum_ctg launch");
+        MPPI_CUDA(launch_finalize_ctg(c, nullptr, nullptr, c.d_commbuf), "finalize_ctg (partials) launch");
+        r = nccl_sum_buf(c, c.d_commbuf, (size_t)c.T + (size_t)c.T * c.m);
+        if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(SUM [eta_t, A]): %s", nccl_error(r));
+        MPPI_CUDA(launch_finalize_ctg(c, U, c.d_commbuf, nullptr), "finalize_ctg (apply) launch");
+        c.last_eps = eps;
+        return MPPI_OK;
+    }
     MPPI_CUDA(launch_wsum(c, eps, &c.d_stats->min_key), "wsum_kernel launch");
     MPPI_CUDA(launch_finalize(c, nullptr, c.d_commbuf, nullptr), "finalize (partials) launch");
     r = nccl_sum_buf(c, c.d_commbuf, (size_t)1 + (size_t)c.T * c.m);
@@ -707,7 +720,7 @@ mppi_status_t mppi_nccl_attach(mppi_ctx* ctx, const uint8_t* id) {
     if (!id) return fail(MPPI_ERR_INVALID_ARG, "id is NULL");
     if (c.nccl) return fail(MPPI_ERR_INVALID_ARG, "a communicator is already attached");
     if (!c.d_commbuf)
-        if (mppi_status_t a = dalloc(c, &c.d_commbuf, (size_t)1 + (size_t)c.T * c.m, "comm buffer")) return a;
+        if (mppi_status_t a = dalloc(c, &c.d_commbuf, (size_t)c.T + (size_t)c.T * c.m, "comm buffer")) return a;
     const int r = nccl_attach(c, id);
     if (r) return fail(MPPI_ERR_NCCL, "ncclCommInitRank(world %d, rank %d): %s", c.world, c.rank, nccl_error(r));
     free_graphs(c);
@@ -735,7 +748,6 @@ mppi_status_t mppi_set_weighting(mppi_ctx* ctx, mppi_weighting_t mode) {
     if (mode != MPPI_WEIGHTS_TRAJECTORY && mode != MPPI_WEIGHTS_COST_TO_GO)
         return fail(MPPI_ERR_INVALID_ARG, "unknown weighting %d", (int)mode);
     if (mode == MPPI_WEIGHTS_COST_TO_GO && !c.d_ctg) {
-        if (c.world != 1) return fail(MPPI_ERR_UNSUPPORTED, "cost-to-go weighting needs world == 1");
         const int64_t nblk = (c.K_loc + 255) / 256;
         mppi_status_t a;
         if ((a = dalloc(c, &c.d_ctg, (size_t)c.T * c.K_loc, "cost-to-go")) ||
@@ -856,6 +868,8 @@ mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, floa
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
     if (!buf) return fail(MPPI_ERR_INVALID_ARG, "buf is NULL");
+    if (c.ctg) return fail(MPPI_ERR_UNSUPPORTED, "the split phase uses trajectory weights; with cost-to-go "
+                           "weighting shard through mppi_nccl_attach + mppi_optimize");
     if (mppi_status_t s = sticky_check(c)) return s;
     c.last_launches = 0;
     const long long* key = global_min_key ? (const long long*)global_min_key : &c.d_stats->min_key;

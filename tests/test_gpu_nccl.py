@@ -40,6 +40,30 @@ def test_single_rank_nccl_equals_direct(cfg, K):
     b.close()
 
 
+@pytest.mark.parametrize("cfg,K", [("C2", 4096), ("C4", 65536)])
+def test_single_rank_nccl_cost_to_go_equals_direct(cfg, K):
+    """NEXT-1 sharded: MIN over the per-step minima and SUM over [eta_t, A] through the library's
+    communicator; one rank reproduces the direct cost-to-go step bit for bit."""
+    w = get(cfg)
+    a = from_workload(w, K=K)
+    b = from_workload(w, K=K)
+    a.set_weighting(True)
+    b.set_weighting(True)
+    b.attach_nccl()
+    Ua = torch.tensor(w.U0, device="cuda")
+    Ub = Ua.clone()
+    for i in range(3):
+        a.optimize(w.x0, Ua, w.seed, i)
+        b.optimize(w.x0, Ub, w.seed, i)
+    torch.cuda.synchronize()
+    assert torch.equal(Ua, Ub)
+    assert a.stats() == b.stats()
+    with pytest.raises(MppiError):                  # the split phase is trajectory-only
+        b.accumulate()
+    a.close()
+    b.close()
+
+
 def test_world2_optimize_needs_communicator():
     w = get("C1")
     m = from_workload(w, K=1024, rank=0, world=2)
