@@ -34,7 +34,7 @@ ROLLOUT_FLOP_PER_SS = {"cartpole": 59.43, "racecar": 251.49,  # profiles/r1_roll
                        "quadrotor": 464.56}  # profiles/r1_ncu_full_c5_v7.txt (rollout v7, x2)
 # The packed quadrotor rollout with the obstacle candidate grid and the in-kernel noise (the C5
 # path, K_loc >= 65536): FP32 FLOPs, issued thread instructions and DRAM bytes per sample-step,
-# ncu --set full at C5 (profiles/r1_ncu_full_c5_v9.txt).  The kernel also draws the noise
+# ncu --set full at C5 (profiles/r1_ncu_full_c5_v9.txt, re-captured in v10).  The kernel also draws the noise
 # (Philox integer work, Box-Muller) so it is issue-bound on a mixed integer/FP32 stream; the
 # FP32-pipe fraction is the roofline, the issue-slot fraction is reported beside it.
 FUSED_QUAD = {"flop": 358.59, "inst": 337.49, "dram_bytes": 15.952}
@@ -78,19 +78,37 @@ def parse_args():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML every 10 ms (pynvml,
+    initialised before the region), else nvidia-smi every 200 ms."""
 
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active",
               "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
               "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+    REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
-        self.rows = []
+        self.rows = []          # (sm_mhz, sm_max_mhz, {reasons})
         self.proc = None
         self.thread = None
+        self.stop_flag = threading.Event()
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.sm_max = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self.masks = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                          pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+        except Exception:
+            self.nvml = None
 
     def start(self):
+        if self.nvml is not None:
+            self.thread = threading.Thread(target=self._poll_nvml, daemon=True)
+            self.thread.start()
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits",
@@ -99,32 +117,47 @@ class ClockSampler:
         except Exception:
             self.proc = None
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread = threading.Thread(target=self._read_smi, daemon=True)
         self.thread.start()
 
-    def _read(self):
+    def _poll_nvml(self):
+        nv = self.nvml
+        while not self.stop_flag.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                self.rows.append((float(sm), float(self.sm_max),
+                                  {n for n, m in zip(self.REASONS, self.masks) if bits & m}))
+            except Exception:
+                pass
+            self.stop_flag.wait(0.01)
+
+    def _read_smi(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) == len(self.FIELDS):
-                self.rows.append(parts)
+            if len(parts) == len(self.FIELDS) and parts[0].replace(".", "").isdigit():
+                self.rows.append((float(parts[0]), float(parts[1]) if parts[1].replace(".", "").isdigit() else 0.0,
+                                  {self.REASONS[i] for i in range(4) if parts[3 + i].lower() == "active"}))
 
     def stop(self):
-        if self.proc is None:
+        if self.nvml is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=5)
+        elif self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=5)
+        else:
             return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.thread.join(timeout=5)
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(set().union(*[r[2] for r in self.rows])), "samples": len(self.rows),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------- helpers
