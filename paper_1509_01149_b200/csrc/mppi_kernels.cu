@@ -338,8 +338,13 @@ __device__ __forceinline__ void stage_step_constants(const RolloutArgs<PP>& a, f
 //
 // GEN (diagonal Sigma and R, plants other than the quadrotor, whose large-K path is the packed
 // kernel): eps[t][k] is drawn in step t with K1's counters and transform and written to eps_out.
+// resident CTAs per SM the one-sample kernel is compiled for: the quadrotor (16 states, the
+// obstacle search) needs up to 128 registers; the small plants fit 64
+template <class Plant>
+constexpr int rollout_min_blocks() { return std::is_same<Plant, Quadrotor>::value ? 4 : 8; }
+
 template <class Plant, bool DIAG, int NP, bool GEN = false>
-__global__ void __launch_bounds__(kRolloutThreads, 8)
+__global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
     rollout_kernel(const __grid_constant__ RolloutArgs<typename Plant::Params> a) {
     constexpr int M = Plant::M;
     extern __shared__ float4 smem4[];
@@ -347,9 +352,17 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
     StepRec* sRec = reinterpret_cast<StepRec*>(smem4 + a.n_obs_pairs);   // per-t constants [T]
     float* sRing = reinterpret_cast<float*>(sRec + a.T);               // eps ring [kEpsStages][blockDim][M]
     // general path: per-t sampling factor F_t and IS matrix G_t after the ring ([T][2][M*M])
-    float* sMat = sRing + kEpsStages * blockDim.x * M;
+    float* sMat = sRing + (GEN ? 0 : kEpsStages * blockDim.x * M);
+    // candidate grid (NP == kCellGrid, diagonal path only): centres and cell words
+    float2* sCent = reinterpret_cast<float2*>(sMat);
+    uint32_t* sCells = reinterpret_cast<uint32_t*>(sCent + a.n_cent);
     const int tid = threadIdx.x;
     stage_step_constants<M, DIAG>(a, sObs, sRec, sMat);
+    if constexpr (NP == kCellGrid) {
+        for (int i = tid; i < a.n_cent; i += blockDim.x) sCent[i] = a.cent[i];
+        const int nc = a.cell_nx * a.cell_ny;
+        for (int i = tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
+    }
     __syncthreads();
     pdl_wait();                        // eps and the min-key reset of the noise pass
 
@@ -358,7 +371,17 @@ __global__ void __launch_bounds__(kRolloutThreads, 8)
     if (k < a.K_loc) {
         // compile-time pair count: read the forest from the kernel-parameter constant bank
         // (uniform-register operands, no per-thread registers); else shared memory
-        const ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
+        ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
+        if constexpr (NP == kCellGrid) {
+            ob.cells = sCells;
+            ob.cent = sCent;
+            ob.nx = a.cell_nx;
+            ob.ny = a.cell_ny;
+            ob.ox = a.cell_ox;
+            ob.oy = a.cell_oy;
+            ob.inv_h = a.cell_inv_h;
+            ob.band = a.cell_band;
+        }
         ScalarRollout<Plant, DIAG, NP> ro(a, ob, sMat, k);
         const size_t row = (size_t)a.K_loc * M;
         const StepRec* rec = sRec;
@@ -1550,7 +1573,7 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     const void* kern;
     if constexpr (X2) {
         kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
-    } else if constexpr (DIAG && !std::is_same<Plant, Quadrotor>::value) {
+    } else if constexpr (DIAG && (!std::is_same<Plant, Quadrotor>::value || NP == kCellGrid)) {
         kern = c.gen_eps ? (const void*)rollout_kernel<Plant, DIAG, NP, true> : (const void*)rollout_kernel<Plant, DIAG, NP>;
     } else {
         if (c.gen_eps) return cudaErrorInvalidValue;   // fused_noise_applies() excludes this variant
@@ -1572,8 +1595,11 @@ template <class Plant, bool DIAG, int NP>
 static cudaError_t dispatch_np(Ctx& c, const typename Plant::Params& P, const float* x0,
                                const float* U, const float* eps, float* costs_out) {
     if constexpr (NP == 0) {
-        if (c.use_cells && c.cell_nx > 0 && c.pack2 && c.K_loc >= kPackedMinK)
-            return launch_rollout_t<Plant, DIAG, kCellGrid, true>(c, P, x0, U, eps, costs_out);
+        if (c.use_cells && c.cell_nx > 0) {
+            if (c.pack2 && c.K_loc >= kPackedMinK)
+                return launch_rollout_t<Plant, DIAG, kCellGrid, true>(c, P, x0, U, eps, costs_out);
+            return launch_rollout_t<Plant, DIAG, kCellGrid>(c, P, x0, U, eps, costs_out);
+        }
     }
     if constexpr (NP > kMaxStaticPairs) {
         if (c.pack2 && c.K_loc >= kPackedMinK) return launch_rollout_t<Plant, DIAG, -1, true>(c, P, x0, U, eps, costs_out);
@@ -1604,7 +1630,8 @@ static cudaError_t launch_rollout_p(Ctx& c, const typename Plant::Params& P, con
 
 bool fused_noise_applies(const Ctx& c) {
     if (!c.fuse_noise || !c.diag || c.per_t) return false;
-    if (c.plant == MPPI_PLANT_QUADROTOR) return c.pack2 && c.K_loc >= kPackedMinK;   // packed kernel
+    if (c.plant == MPPI_PLANT_QUADROTOR)   // packed kernel, or the one-sample grid kernel
+        return c.K_loc >= kPackedMinK && (c.pack2 || (c.use_cells && c.cell_nx > 0));
     // one-sample GEN kernel: only once the step is throughput-bound (measured: -2..4 % at
     // K = 2^20; at small K the per-thread noise lengthens the latency-bound step loop)
     return c.K_loc >= kPackedMinK;
