@@ -241,6 +241,9 @@ mppi_status_t mppi_set_stream(mppi_ctx* ctx, void* cuda_stream);
 /* mppi_optimize — one full MPPI step.  world == 1, or world > 1 with a communicator attached by
  * mppi_nccl_attach (else UNSUPPORTED; the split-phase calls below work without one):
  *   noise -> rollout -> min -> weights + weighted noise sum -> U update.
+ * Kernels: K1 noise (or drawn inside K2, MPPI_OPTION_FUSED_NOISE), K2 rollout (+ CTA min and
+ * int64 atomicMin of the (cost, k) key), K3 weights + weighted noise sum per chunk, K4 fixed-order
+ * chunk sum and update; with a communicator the two allreduces sit between K2/K3 and K3/K4.
  *   x0    : HOST float [n], the current state x_{t0}; read before return (passed by value).
  *   U     : DEVICE float [T][m], the nominal control sequence, updated in place.
  *   seed, step : Philox key and counter words; eps[t][k][j] = j-th normal of
@@ -248,7 +251,8 @@ mppi_status_t mppi_set_stream(mppi_ctx* ctx, void* cuda_stream);
  *           by the fixed fp32 Box-Muller sequence of SURVEY.md Appendix B.
  *   noise : NULL -> generate eps as above into the context; otherwise DEVICE float [T][K][m]
  *           of N(0,1) samples supplied by the caller (seed/step ignored), read-only.
- * Errors: INVALID_ARG (NULL U, non-finite x0), UNSUPPORTED (world > 1), CUDA. */
+ * Errors: INVALID_ARG (NULL U, non-finite x0), UNSUPPORTED (world > 1 without a communicator),
+ * NCCL, CUDA. */
 mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed,
                             uint64_t step, const float* noise);
 
@@ -434,9 +438,10 @@ int32_t mppi_last_launch_count(const mppi_ctx* ctx);
 
 typedef enum {
     MPPI_KERNEL_NOISE = 0,     /* K1 noise_kernel */
-    MPPI_KERNEL_ROLLOUT = 1,   /* K2 rollout_kernel */
-    MPPI_KERNEL_WSUM = 2,      /* K3 wsum_kernel (weights + weighted noise sum) */
-    MPPI_KERNEL_FINALIZE = 3,  /* K4 finalize_kernel (partials -> [eta, A] -> U) */
+    MPPI_KERNEL_ROLLOUT = 1,   /* K2 rollout_kernel / rollout_kernel_x2 (incl. in-kernel noise) */
+    MPPI_KERNEL_WSUM = 2,      /* K3 wsum (weights + weighted noise sum; cost-to-go: also the
+                                  suffix-sum and per-step minimum passes) */
+    MPPI_KERNEL_FINALIZE = 3,  /* K4 finalize (partials -> [eta, A] -> U) */
     MPPI_KERNEL_SHIFT = 4,     /* K5 shift_kernel */
     MPPI_KERNEL_KINDS = 5
 } mppi_kernel_kind_t;
