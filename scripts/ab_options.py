@@ -17,7 +17,7 @@ for spec in sys.argv[1:]:
         m.set_weighting(True)
     for kv in filter(None, spec.split(",")):
         k, v = kv.split("=")
-        m.set_option(getattr(A, "MPPI_OPTION_" + k), int(v))
+        m.set_option(int(k) if k.isdigit() else getattr(A, "MPPI_OPTION_" + k), int(v))
     U = torch.tensor(w.U0, device="cuda")
     for i in range(3):
         m.optimize(w.x0, U, w.seed, i)
