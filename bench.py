@@ -274,15 +274,17 @@ def latency(cfg_name, iters=200, warm=20):
 
 
 # ----------------------------------------------------------------------------- other configs
-def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False):
+def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=False):
     """K*T/s of one config on this GPU (graph replay, CUDA events around `steps` steps)."""
     import torch
     from mppi_inputs import get
-    from paper_1509_01149_b200 import from_workload
+    from paper_1509_01149_b200 import _capi as A, from_workload
     w = get(cfg_name)
     m = from_workload(w, K=K or w.K)
     if cost_to_go:
         m.set_weighting(True)
+    if sparse:
+        m.set_option(A.MPPI_OPTION_SPARSE_REDUCTION, 1)
     U = torch.tensor(w.U0, device="cuda")
     for i in range(warm):
         m.optimize(w.x0, U, w.seed, i)
@@ -297,7 +299,8 @@ def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False):
     m.close()
     return {"plant": w.plant, "K": K or w.K, "T": w.T, "ms_per_step": ms,
             "KT_per_s": (K or w.K) * w.T / (ms * 1e-3),
-            "weighting": "cost-to-go (PAPER.md:320-322)" if cost_to_go else "trajectory"}
+            "weighting": "cost-to-go (PAPER.md:320-322)" if cost_to_go else "trajectory",
+            "reduction": "sparse (all-zero weight blocks skipped, bit-identical)" if sparse else "dense GEMV"}
 
 
 def closed_loop(cfg_name="C2"):
@@ -560,6 +563,7 @@ def main():
         extra = {"configs": {c: throughput(c) for c in ("C3", "C4")},
                  "C5_sweep": [throughput("C5", K=1 << e, steps=5) for e in (16, 18, 20, 22)],
                  "C5_cost_to_go": throughput("C5", steps=5, cost_to_go=True),
+                 "C5_sparse_reduction": throughput("C5", steps=5, sparse=True),
                  "closed_loop": closed_loop("C2"),
                  "device_closed_loop": device_closed_loop("C2"),
                  "fig1_trend": fig1_trend()}

@@ -280,12 +280,20 @@ typedef enum {
                                           shared-memory ring filled by bulk copies (cp.async.bulk
                                           + mbarrier) instead of per-thread loads; identical
                                           results (default 1) */
-    MPPI_OPTION_PDL = 6                /* the step's CUDA graph links its kernels with programmatic
+    MPPI_OPTION_PDL = 6,               /* the step's CUDA graph links its kernels with programmatic
                                           (dependent-launch) edges: a kernel's CTAs launch as the
                                           previous kernel's last CTAs exit and wait
                                           (griddepcontrol.wait) for its results; identical results.
                                           Default 0: on B200 it saves ~1.5 us of p50 latency at
                                           C1-C3 but adds ~10 us to the C1 p99 */
+    MPPI_OPTION_SPARSE_REDUCTION = 7   /* with the bulk-copy reduction and K_loc >= 65536: a pass over the costs flags the
+                                          256-column blocks holding a nonzero fp32 weight and the
+                                          weighted noise sum streams only those (zero weights add
+                                          exact zeros: identical results).  With small lambda the
+                                          weights are nearly one-hot (C1-C5: one nonzero weight), and
+                                          the reduction then reads kilobytes instead of 4 T K m bytes.
+                                          Default 0: bench.py measures the dense GEMV the north_star
+                                          defines and reports this mode beside it */
 } mppi_option_t;
 
 /* mppi_set_option — execution options that never change results. */

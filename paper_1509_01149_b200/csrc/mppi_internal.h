@@ -90,6 +90,8 @@ struct Ctx {
     bool fuse_noise = true;         // packed rollout draws its own noise (no K1 pass)
     bool tma_wsum = true;           // K3 streams eps with bulk copies (MPPI_OPTION_BULK_REDUCTION)
     bool use_pdl = false;           // programmatic kernel->kernel edges in the step graph (MPPI_OPTION_PDL)
+    bool sparse_wsum = false;       // K3 skips all-zero-weight column blocks (MPPI_OPTION_SPARSE_REDUCTION)
+    uint8_t* d_flags = nullptr;     // [ceil(K_loc m / 4 / 256)] nonzero-weight block flags
     // set around a fused launch: the rollout writes the noise it draws here (else nullptr)
     float* gen_eps = nullptr;
     uint64_t gen_seed = 0, gen_step = 0;

@@ -588,6 +588,7 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
 
 // ------------------------------------------------------------------------------ K3 weights + GEMV
 struct WsumArgs {
+    const uint8_t* flags;       // wsum_tma_kernel: per 256-column block "some weight != 0", or nullptr
     const float* eps;           // [T][K_loc][M] viewed as [T][ncols] float4
     const float* costs;         // [K_loc]
     const long long* key;       // global min key
@@ -682,6 +683,26 @@ __global__ void __launch_bounds__(kWsumThreads) wsum_kernel(const WsumArgs a) {
     }
 }
 
+// Sparse K3 (MPPI_OPTION_SPARSE_REDUCTION): flags[b] = 1 iff some sample of the 256-column block
+// b has a nonzero fp32 weight exp(-(S - S_min)/lambda) (the exact expression K3 evaluates).
+// With small lambda the weights are mostly exact zeros (C1-C5: one nonzero weight), and K3 then
+// streams only the flagged blocks.
+template <int M>
+__global__ void __launch_bounds__(kWsumThreads) wsum_flags_kernel(const WsumArgs a) {
+    pdl_wait();
+    constexpr int SPC = 4 / M;
+    const float smin = key_cost(*a.key);
+    const long long col = (long long)blockIdx.x * kWsumThreads + threadIdx.x;
+    int nz = 0;
+    if (col < a.ncols) {
+#pragma unroll
+        for (int s2 = 0; s2 < SPC; ++s2)
+            nz |= expf(-__fdiv_rn(__ldg(a.costs + col * SPC + s2) - smin, a.lambda)) != 0.0f;
+    }
+    nz = __syncthreads_or(nz);
+    if (threadIdx.x == 0) const_cast<uint8_t*>(a.flags)[blockIdx.x] = (uint8_t)(nz != 0);
+}
+
 // K3 with the bulk-copy engine (sm_90+ cp.async.bulk, SASS UBLKCP): the same partial sums, but
 // the eps tiles stream into a kWsumStages-deep shared-memory ring filled by one thread with 1-D
 // bulk copies (one per timestep row, CW float4 columns) and mbarrier completion, so the bytes in
@@ -748,25 +769,35 @@ __global__ void __launch_bounds__(kWsumThreads, 3) wsum_tma_kernel(const WsumArg
     __syncthreads();
     pdl_wait();                        // costs, key and eps of the rollout
     const float smin = key_cost(*a.key);
-    auto issue = [&](long long j) {
-        const int st = (int)(j % S);
+    // sparse mode: blocks whose every weight is exactly 0 (flags[] == 0) are skipped by producer
+    // and consumers alike; they would add exact zeros, so the sums are bit-identical
+    const uint8_t* flags = a.flags ? a.flags + c_begin / CW : nullptr;
+    auto flagged = [&](long long j) -> bool { return !flags || flags[j] != 0; };
+    auto issue = [&](long long j, int st) {
         const long long c0 = c_begin + j * CW;
         const unsigned bytes = (unsigned)(min((long long)CW, c_end - c0) * sizeof(float4));
         mbar_expect_tx(&full[st], bytes * nt);
         for (int tt = 0; tt < nt; ++tt)
             bulk_g2s(sbuf + ((size_t)st * TT + tt) * CW, eps4 + (size_t)(t0 + tt) * a.ncols + c0, bytes, &full[st]);
     };
-    if (tid == 0)
-        for (long long j = 0; j < nblk && j < S; ++j) issue(j);
+    long long jp = 0;                  // producer (thread 0): next block to look at
+    if (tid == 0) {
+        int n = 0;
+        for (; jp < nblk && n < S; ++jp)
+            if (flagged(jp)) issue(jp, n++);
+    }
     float acc[TT][4];
 #pragma unroll
     for (int tt = 0; tt < TT; ++tt)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[tt][c] = 0.0f;
     float eta = 0.0f;
+    long long used = 0;                // ring slots consumed
     for (long long j = 0; j < nblk; ++j) {
-        const int st = (int)(j % S);
-        const unsigned parity = (unsigned)((j / S) & 1);
+        if (!flagged(j)) continue;
+        const int st = (int)(used % S);
+        const unsigned parity = (unsigned)((used / S) & 1);
+        ++used;
         const long long col = c_begin + j * CW + tid;
         const bool valid = col < c_end;
         float w[SPC];
@@ -803,9 +834,12 @@ __global__ void __launch_bounds__(kWsumThreads, 3) wsum_tma_kernel(const WsumArg
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
-        if (tid == 0 && j + S < nblk) {
-            mbar_wait(&empty[st], parity);   // every warp is done with block j: refill its slot
-            issue(j + S);
+        if (tid == 0) {
+            while (jp < nblk && !flagged(jp)) ++jp;
+            if (jp < nblk) {
+                mbar_wait(&empty[st], parity);   // every warp is done with this slot: refill it
+                issue(jp++, st);
+            }
         }
     }
     __shared__ float red[NW][TT * M + 1];
@@ -1662,6 +1696,7 @@ cudaError_t launch_rollout(Ctx& c, const float* x0, const float* U, const float*
 
 cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key) {
     WsumArgs a;
+    a.flags = nullptr;
     a.eps = eps;
     a.costs = c.d_costs;
     a.key = key;
@@ -1676,6 +1711,14 @@ cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key) {
         const void* f = c.m == 1 ? (const void*)wsum_tma_kernel<1> : c.m == 2 ? (const void*)wsum_tma_kernel<2>
                       : c.m == 4 ? (const void*)wsum_tma_kernel<4> : nullptr;
         if (!f) return cudaErrorInvalidValue;
+        if (c.sparse_wsum && c.d_flags && c.K_loc >= kPackedMinK) {   // (small K: the extra pass costs more)
+            a.flags = c.d_flags;
+            const void* ff = c.m == 1 ? (const void*)wsum_flags_kernel<1> : c.m == 2 ? (const void*)wsum_flags_kernel<2>
+                           : (const void*)wsum_flags_kernel<4>;
+            const unsigned nb = (unsigned)((a.ncols + kWsumThreads - 1) / kWsumThreads);
+            cudaError_t e = emit(c, ff, dim3(nb), dim3(kWsumThreads), 0, &a, sizeof(a), MPPI_KERNEL_WSUM);
+            if (e != cudaSuccess) return e;
+        }
         const size_t smem = kWsumTmaSmem;
         cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

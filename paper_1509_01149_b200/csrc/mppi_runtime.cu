@@ -301,6 +301,7 @@ void free_ctx(Ctx& c) {
     cudaFree(c.d_obs);
     cudaFree(c.d_cells);
     cudaFree(c.d_cent);
+    cudaFree(c.d_flags);
     cudaFree(c.d_eps);
     cudaFree(c.d_costs);
     cudaFree(c.d_key_init);
@@ -495,6 +496,7 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
         (a = dalloc(c, &c.d_stats, 1, "stats")) ||
         (a = dalloc(c, &c.d_U, (size_t)T * m, "U staging")) ||
         (a = dalloc(c, &c.d_obs, (size_t)(c.n_obs_pairs > 0 ? c.n_obs_pairs : 1), "obstacles")) ||
+        (a = dalloc(c, &c.d_flags, (size_t)((ncols + kWsumThreads - 1) / kWsumThreads), "weight block flags")) ||
         (!c.cells_host.empty() &&
          ((a = dalloc(c, &c.d_cells, c.cells_host.size(), "obstacle grid")) ||
           (a = dalloc(c, &c.d_cent, c.cent_host.size(), "obstacle centres"))))) {
@@ -665,6 +667,7 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
         case MPPI_OPTION_FUSED_NOISE: ctx->c.fuse_noise = value != 0; return MPPI_OK;
         case MPPI_OPTION_OBSTACLE_GRID: ctx->c.use_cells = value != 0; return MPPI_OK;
         case MPPI_OPTION_BULK_REDUCTION: ctx->c.tma_wsum = value != 0; return MPPI_OK;
+        case MPPI_OPTION_SPARSE_REDUCTION: ctx->c.sparse_wsum = value != 0; return MPPI_OK;
         case MPPI_OPTION_PDL:
             MPPI_CUDA(cudaStreamSynchronize(ctx->c.stream), "stream sync");
             ctx->c.use_pdl = value != 0;

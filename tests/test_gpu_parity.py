@@ -470,6 +470,31 @@ def test_pdl_graph_is_bitwise_plain_graph(cfg, K):
     b.close()
 
 
+@pytest.mark.parametrize("cfg,K,lam", [("C4", 65536, None), ("C4", 65536 + 4, 30.0), ("C4", 1 << 18, 1e4),
+                                        ("C3", 16384, 2.0), ("C1", 1000, None)])
+def test_sparse_reduction_is_bitwise_dense(cfg, K, lam):
+    """MPPI_OPTION_SPARSE_REDUCTION: skipping the 256-column blocks whose weights are all exactly
+    zero gives the dense reduction's bits (one-hot weights at the configs' lambda; partly and
+    fully dense weights at larger lambda)."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get(cfg)
+    if lam is not None:
+        w.lam = lam
+    a = from_workload(w, K=K)
+    b = from_workload(w, K=K)
+    a.set_option(A.MPPI_OPTION_SPARSE_REDUCTION, 1)
+    for graph in (True, False):
+        a.use_graph(graph)
+        Ua, Ub = cuda_u(w), cuda_u(w)
+        for i in range(3):
+            a.optimize(w.x0, Ua, 8, i)
+            b.optimize(w.x0, Ub, 8, i)
+        torch.cuda.synchronize()
+        assert torch.equal(Ua, Ub) and a.stats() == b.stats()
+    a.close()
+    b.close()
+
+
 @pytest.mark.parametrize("xy", [(0.0, 0.0), (25.0, 1.5), (44.0, -9.0), (300.0, 0.0), (-60.0, 80.0), (5000.0, 5.0)])
 def test_obstacle_grid_is_bitwise_full_search(xy):
     """MPPI_OPTION_OBSTACLE_GRID: the per-cell candidate lists give the same nearest-cylinder
