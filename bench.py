@@ -528,6 +528,12 @@ def main():
         if fused:   # issue-slot utilisation: 1 warp instruction / cycle / SM sub-partition
             slots = props.multi_processor_count * 4 * sm_max * 1e6
             roof["issue_frac"] = FUSED_QUAD["inst"] / 32.0 * units / avg_s / slots
+            # the FP32 work of the same step done the direct way (full 50-cylinder search, noise
+            # read from HBM: the v7 kernel's ncu count) over this kernel's time -- an effective
+            # rate, not executed FLOPs
+            eff = ROLLOUT_FLOP_PER_SS["quadrotor"] * units / avg_s / 1e12
+            roof["effective_full_search"] = {"tflops": eff, "frac": eff / fp["peak_tflops"],
+                                             "flop_per_sample_step": ROLLOUT_FLOP_PER_SS["quadrotor"]}
     else:
         algo = 4.0 * w.T * K_loc * w.m + 4.0 * K_loc if dom == "wsum" else 4.0 * w.T * K_loc * w.m
         peak = pk.get("hbm_gbs", 6650.0)
