@@ -273,6 +273,13 @@ def latency(cfg_name, iters=200, warm=20):
             "KT_per_s_at_p50": w.K * w.T / (q(dev, 0.5) * 1e-6)}
 
 
+def _safe(fn, *a, **k):
+    try:
+        return fn(*a, **k)
+    except Exception as e:          # an extra must not sink the bench line
+        return {"error": str(e)[:200]}
+
+
 # ----------------------------------------------------------------------------- other configs
 def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=False):
     """K*T/s of one config on this GPU (graph replay, CUDA events around `steps` steps)."""
@@ -301,6 +308,28 @@ def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=Fals
             "KT_per_s": (K or w.K) * w.T / (ms * 1e-3),
             "weighting": "cost-to-go (PAPER.md:320-322)" if cost_to_go else "trajectory",
             "reduction": "sparse (all-zero weight blocks skipped, bit-identical)" if sparse else "dense GEMV"}
+
+
+def c_abi_closed_loop(steps=200):
+    """examples/cartpole_mpc.c (config C2 from plain C through the ABI): control-update wall time
+    p50/p99 per mppi_optimize_host call (x0 and U in, the step, U out) and the swing-up result."""
+    import shutil
+    import tempfile
+    from paper_1509_01149_b200 import build as B
+    gcc = shutil.which("gcc") or shutil.which("cc")
+    if gcc is None:
+        return {"error": "no C compiler"}
+    lib = B.build()
+    libdir = os.path.dirname(lib)
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "cartpole_mpc")
+        subprocess.run([gcc, "-O2", "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "examples", "cartpole_mpc.c"),
+                        "-L", libdir, "-lmppi_b200", "-Wl,-rpath," + libdir, "-lm", "-o", exe], check=True)
+        out = subprocess.run([exe, str(steps)], capture_output=True, text=True, timeout=300, check=True).stdout.split()
+    val = lambda k: float(out[out.index(k) + 1])
+    return {"config": "C2", "steps": steps, "update_us_p50": val("update_us_p50"),
+            "update_us_p99": val("update_us_p99"), "final_1_plus_cos_theta": val("1+cos(theta)"),
+            "mean_q": val("q"), "api": "mppi_optimize_host from C (examples/cartpole_mpc.c)"}
 
 
 def closed_loop(cfg_name="C2"):
@@ -570,6 +599,7 @@ def main():
                  "C5_sweep": [throughput("C5", K=1 << e, steps=5) for e in (16, 18, 20, 22)],
                  "C5_cost_to_go": throughput("C5", steps=5, cost_to_go=True),
                  "C5_sparse_reduction": throughput("C5", steps=5, sparse=True),
+                 "c_abi_closed_loop": _safe(c_abi_closed_loop),
                  "closed_loop": closed_loop("C2"),
                  "device_closed_loop": device_closed_loop("C2"),
                  "fig1_trend": fig1_trend()}

@@ -7,14 +7,27 @@
  * Build (from the repository root, after python -m paper_1509_01149_b200.build):
  *   gcc -O2 -Iinclude examples/cartpole_mpc.c -Lpaper_1509_01149_b200 -lmppi_b200 \
  *       -Wl,-rpath,$PWD/paper_1509_01149_b200 -lm -o cartpole_mpc
- * Run: ./cartpole_mpc [steps]   (prints the final 1 + cos(theta): ~0 = upright)
+ * Run: ./cartpole_mpc [steps]   (prints the final 1 + cos(theta): ~0 = upright, and the p50 / p99
+ * wall time of one control update: x0 in, U through the step, U out, from host buffers)
  */
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #include "mppi.h"
+
+static double now_us(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
+}
+
+static int cmp_double(const void* a, const void* b) {
+    const double x = *(const double*)a, y = *(const double*)b;
+    return (x > y) - (x < y);
+}
 
 #define K 4096
 #define T 100
@@ -46,8 +59,12 @@ int main(int argc, char** argv) {
     float U[T] = {0};
     float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};      /* hanging at rest */
     double qsum = 0.0;
+    double* lat = (double*)malloc(sizeof(double) * (steps > 0 ? steps : 1));
     for (int s = 0; s < steps; ++s) {
-        if (mppi_optimize_host(ctx, x, U, 1, (uint64_t)s) != MPPI_OK) {
+        const double t0 = now_us();
+        const mppi_status_t st_opt = mppi_optimize_host(ctx, x, U, 1, (uint64_t)s);
+        lat[s] = now_us() - t0;
+        if (st_opt != MPPI_OK) {
             fprintf(stderr, "mppi_optimize_host: %s\n", mppi_last_error());
             mppi_destroy(ctx);
             return 1;
@@ -60,8 +77,11 @@ int main(int argc, char** argv) {
     }
     mppi_stats_t st;
     mppi_get_stats(ctx, &st);
-    printf("steps %d  final 1+cos(theta) %.6f  mean q %.3f  last S_min %.3f\n", steps,
-           1.0 + cos((double)x[2]), qsum / steps, st.s_min);
+    qsort(lat, steps, sizeof(double), cmp_double);
+    printf("steps %d  final 1+cos(theta) %.6f  mean q %.3f  last S_min %.3f  update_us_p50 %.1f  "
+           "update_us_p99 %.1f\n", steps, 1.0 + cos((double)x[2]), qsum / steps, st.s_min,
+           lat[steps / 2], lat[(int)(0.99 * (steps - 1))]);
+    free(lat);
     mppi_destroy(ctx);
     return 0;
 }

@@ -56,6 +56,7 @@ struct KLaunch {
     dim3 grid, block;
     size_t smem = 0;
     int kind = 0;
+    size_t nargs = 0;
     alignas(16) unsigned char args[2048];
     void* argp[1];
 };
@@ -65,6 +66,7 @@ struct GraphState {
     cudaGraphExec_t exec = nullptr;
     std::vector<cudaGraphNode_t> nodes;   // kernel nodes in launch order
     std::vector<const void*> funcs;
+    std::vector<KLaunch> last;            // the arguments each node was last set to
 };
 
 // Device-side per-step results readable by mppi_get_stats.

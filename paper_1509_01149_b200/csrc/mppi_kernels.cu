@@ -1243,7 +1243,7 @@ __global__ void __launch_bounds__(1024) finalize_ctg_kernel(const FinalizeCtgArg
 
 cudaError_t launch_ctg(Ctx& c) {
     const int nblk = (int)((c.K_loc + 255) / 256);
-    CtgArgs a;
+    CtgArgs a{};
     a.ctg = c.d_ctg;
     a.partmin = c.d_ctg_partmin;
     a.T = c.T;
@@ -1262,7 +1262,7 @@ cudaError_t launch_ctg(Ctx& c) {
 }
 
 cudaError_t launch_wsum_ctg(Ctx& c, const float* eps) {
-    WsumCtgArgs a;
+    WsumCtgArgs a{};
     a.eps = eps;
     a.ctg = c.d_ctg;
     a.smin = c.d_ctg_smin;
@@ -1290,7 +1290,7 @@ cudaError_t launch_wsum_ctg(Ctx& c, const float* eps) {
 }
 
 cudaError_t launch_finalize_ctg(Ctx& c, float* U, const float* buf_in, float* buf_out) {
-    FinalizeCtgArgs a;
+    FinalizeCtgArgs a{};
     a.part = c.d_part;
     a.eta_part = c.d_ctg_eta;
     a.n_chunks = c.n_chunks;
@@ -1367,7 +1367,7 @@ __global__ void __launch_bounds__(1024) advance_kernel(const __grid_constant__ A
 template <class Plant>
 static cudaError_t launch_advance_t(Ctx& c, const typename Plant::Params& P, float* x, float* U,
                                     const float* u_init, float* x_log, float* u_log, float* q_log) {
-    AdvanceArgs<typename Plant::Params> a;
+    AdvanceArgs<typename Plant::Params> a{};
     a.x = x;
     a.U = U;
     a.crashed = &c.d_stats->plant_crashed;
@@ -1438,7 +1438,7 @@ __global__ void __launch_bounds__(256) fk_reduce_kernel(const FkArgs a) {
 }
 
 cudaError_t launch_fk_reduce(Ctx& c, double* part, int nblk) {
-    FkArgs a;
+    FkArgs a{};
     a.costs = c.d_costs;
     a.key = &c.d_stats->min_key;
     a.K_loc = (int)c.K_loc;
@@ -1498,6 +1498,7 @@ cudaError_t emit(Ctx& c, const void* func, dim3 grid, dim3 block, size_t smem, c
         L.block = block;
         L.smem = smem;
         L.kind = kind;
+        L.nargs = size;
         memcpy(L.args, args, size);
         return cudaSuccess;
     }
@@ -1534,7 +1535,7 @@ static PhiloxKeys philox_key_schedule(uint64_t seed) {
 cudaError_t launch_noise(Ctx& c, uint64_t seed, uint64_t step, float* out, bool reset_key) {
     const PhiloxKeys keys = philox_key_schedule(seed);
     const dim3 grid((unsigned)((c.K_loc + 255) / 256), (unsigned)((c.T + kNoiseTT - 1) / kNoiseTT));
-    NoiseArgs a;
+    NoiseArgs a{};
     a.eps = out;
     a.K_loc = (int)c.K_loc;
     a.T = c.T;
@@ -1597,7 +1598,7 @@ static void fill_rollout_args(Ctx& c, const typename Plant::Params& P, const flo
 template <class Plant, bool DIAG, int NP, bool X2 = false>
 static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, const float* x0,
                                     const float* U, const float* eps, float* costs_out) {
-    RolloutArgs<typename Plant::Params> a;
+    RolloutArgs<typename Plant::Params> a{};
     fill_rollout_args<Plant>(c, P, x0, U, eps, costs_out, a);
     const int spt = X2 ? 2 : 1;                                      // samples per thread
     const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
@@ -1695,7 +1696,7 @@ cudaError_t launch_rollout(Ctx& c, const float* x0, const float* U, const float*
 }
 
 cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key) {
-    WsumArgs a;
+    WsumArgs a{};
     a.flags = nullptr;
     a.eps = eps;
     a.costs = c.d_costs;
@@ -1741,7 +1742,7 @@ int wsum_blocks_per_sm(int m) {
 }
 
 cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* U) {
-    FinalizeArgs a;
+    FinalizeArgs a{};
     a.part = c.d_part;
     a.eta_part = c.d_eta_part;
     a.n_chunks = c.n_chunks;
@@ -1773,7 +1774,7 @@ cudaError_t launch_shift(Ctx& c, float* U, const float* u_init) {
         if (e != cudaSuccess) return e;
     }
     const int threads = c.T * c.m >= 1024 ? 1024 : ((c.T * c.m + 31) / 32) * 32;
-    ShiftArgs a;
+    ShiftArgs a{};
     a.U = U;
     a.T = c.T;
     a.M = c.m;

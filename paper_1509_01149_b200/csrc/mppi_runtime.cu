@@ -638,14 +638,22 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
             }
             G.nodes.push_back(node);
             G.funcs.push_back(L.func);
+            G.last.push_back(L);
             prev = node;
             prev_is_kernel = true;
         }
         MPPI_CUDA(cudaGraphInstantiate(&G.exec, G.graph, 0), "cudaGraphInstantiate");
     } else {
         for (size_t i = 0; i < c.pending.size(); ++i) {
-            cudaKernelNodeParams p = node_params(c.pending[i]);
+            KLaunch& L = c.pending[i];
+            const KLaunch& O = G.last[i];
+            // most calls change only x0 / seed / step: skip the nodes whose arguments are unchanged
+            if (L.nargs == O.nargs && memcmp(L.args, O.args, L.nargs) == 0 && L.smem == O.smem &&
+                L.grid.x == O.grid.x && L.grid.y == O.grid.y && L.grid.z == O.grid.z && L.block.x == O.block.x)
+                continue;
+            cudaKernelNodeParams p = node_params(L);
             MPPI_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, G.nodes[i], &p), "graph node update");
+            G.last[i] = L;
         }
     }
     MPPI_CUDA(cudaGraphLaunch(G.exec, c.stream), "cudaGraphLaunch");
