@@ -230,19 +230,22 @@ def test_determinism():
         assert torch.equal(c, outs[0][0]) and torch.equal(U, outs[0][1]) and k == outs[0][2]
 
 
-def test_sharded_split_phase_matches_single_gpu():
-    """P13 emulated on one GPU (SURVEY §4 "fake backend"): G contexts with rank/world run their
-    shards; the host combines MIN of keys and SUM of [eta, A]; costs and noise are bitwise the
-    single-GPU ones and U agrees within 1e-6."""
+@pytest.mark.parametrize("K", [8192, 1 << 19])
+def test_sharded_split_phase_matches_single_gpu(K):
+    """P13 emulated on one GPU (SURVEY §4 "fake backend"): G = 2, 4, 8 contexts with rank/world
+    run their shards; the host combines MIN of keys and SUM of [eta, A]; noise, costs and k* are
+    bitwise the single-GPU ones and U agrees within 1e-6.  K = 2^19 puts every shard of G <= 8 on
+    the packed kernels with in-kernel noise (K_loc >= 65536)."""
     w = get("C4")
-    K = 8192
     single = from_workload(w, K=K)
     U1 = cuda_u(w)
     c1, k1 = single.rollout_costs(w.x0, U1, 4, 1)
     c1 = c1.clone()
+    eps1 = single.noise(4, 1)
     single.optimize(w.x0, U1, 4, 1)
-    for G in (2, 4):
+    for G in (2, 4, 8):
         ms = [from_workload(w, K=K, rank=r, world=G) for r in range(G)]
+        assert torch.equal(torch.cat([m.noise(4, 1) for m in ms], dim=1), eps1)
         U = cuda_u(w)
         outs = [m.rollout_costs(w.x0, U, 4, 1) for m in ms]
         costs = torch.cat([o[0] for o in outs])
@@ -259,6 +262,8 @@ def test_sharded_split_phase_matches_single_gpu():
         for Ur in Us[1:]:
             assert torch.equal(Ur, Us[0])
         assert torch.max(torch.abs(Us[0] - U1)).item() <= 1e-6
+        for m in ms:
+            m.close()
 
 
 def test_penalty_on_non_finite_noise():
