@@ -227,13 +227,24 @@ struct ScalarRollout {
     Plant st;
     float S = 0.0f;
     float is_prev = 0.0f;                                              // IS term of step t-1
+    bool slow = false;                                                 // a fast-path range miss
 
     __device__ __forceinline__ ScalarRollout(const RolloutArgs<typename Plant::Params>& a_, const ObstacleView& ob_,
                                              const float* sMat_, int k_)
         : a(a_), ob(ob_), sMat(sMat_), k(k_) {
-        st.load(a.x0_dev ? a.x0_dev : a.x0, 0);
+        reset();
     }
 
+    __device__ __forceinline__ void reset() {
+        st.load(a.x0_dev ? a.x0_dev : a.x0, 0);
+        S = 0.0f;
+        is_prev = 0.0f;
+    }
+
+    // SAFE = false (the hot loop): the fast transcendental path only, recording in `slow`
+    // whether an argument left its range (no branch in the step body); SAFE = true (replay()):
+    // the per-step accurate fallback.
+    template <bool SAFE = false>
     __device__ __forceinline__ void step(const StepRec* rec, const float* e, bool first, int t) {
         const float4 u4 = rec->u;
         const float4 b4 = rec->b;
@@ -271,9 +282,13 @@ struct ScalarRollout {
         }
         // rotated step: q(x_t) (the cost of step t-1, 0 at t = 0) and F(x_t, v_t) only need
         // x_t, so they share one basic block; then x_{t+1} = x_t + F dt
-        const float q = st.template state_cost<NP>(first, a.P, ob);
+        const float q = st.template state_cost<NP, SAFE>(first, a.P, ob);
         float xd[Plant::N];
-        if (st.deriv_fast(v, a.P, xd)) st.deriv_accurate(v, a.P, xd);   // |angle| > 105615: rare
+        if constexpr (SAFE) {
+            if (st.deriv_fast(v, a.P, xd)) st.deriv_accurate(v, a.P, xd);   // |angle| > 105615: rare
+        } else {
+            slow |= st.deriv_fast(v, a.P, xd);
+        }
         st.update(xd, a.dt);
         S += q + is;                                                   // S~ += q~
         if (a.qstep) {                                                 // q~_{t-1} = q(x_t) + IS_{t-1}
@@ -282,9 +297,23 @@ struct ScalarRollout {
         }
     }
 
+    // the trajectory again from x0 with the per-step accurate fallback, reading back the noise
+    // the hot loop used (eps: the rows it read or wrote): the inline-fallback semantics
+    __device__ __forceinline__ void replay(const float* eps, const StepRec* rec) {
+        reset();
+        const size_t row = (size_t)a.K_loc * M;
+        const float* ep = eps + (size_t)k * M;
+        for (int t = 0; t < a.T; ++t, ++rec, ep += row) {
+            float e[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) e[i] = ep[i];
+            step<true>(rec, e, t == 0, t);
+        }
+    }
+
     // + q(x_T) (the cost of step T-1); non-finite -> penalty
     __device__ __forceinline__ float finish() {
-        const float qT = st.template state_cost<NP>(false, a.P, ob);
+        const float qT = st.template state_cost<NP, true>(false, a.P, ob);
         S += qT;
         if (a.qstep) a.qstep[(size_t)(a.T - 1) * a.K_loc + k] = qT + is_prev;
         if (!isfinite(S)) S = a.penalty;
@@ -397,6 +426,7 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
         } else {
             eps_ring_loop<M>(a.eps, row, a.T, k, sRing, [&](int t, const float* e) { ro.step(rec++, e, t == 0, t); });
         }
+        if (__builtin_expect(ro.slow, 0)) ro.replay(GEN ? a.eps_out : a.eps, sRec);
         const float S = ro.finish();
         a.costs[k] = S;
         if (a.costs_out) a.costs_out[k] = S;
@@ -1345,10 +1375,10 @@ __global__ void __launch_bounds__(1024) advance_kernel(const __grid_constant__ A
 #pragma unroll
         for (int i = 0; i < M; ++i) u0[i] = sUa[i];
         float xd[Plant::N];
-        st.template state_cost<-1>(true, a.P, ob);
+        st.template state_cost<-1, true>(true, a.P, ob);
         st.deriv_accurate(u0, a.P, xd);
         st.update(xd, a.dt);
-        const float q = st.template state_cost<-1>(false, a.P, ob);
+        const float q = st.template state_cost<-1, true>(false, a.P, ob);
         float xo[16];
         st.store(xo);
         for (int i = 0; i < a.n; ++i) {
@@ -1792,10 +1822,10 @@ static float host_step_t(const Ctx& c, const typename Plant::Params& P, float* x
     st.load(xin, crashed ? *crashed : 0);
     const ObstacleView ob{c.obs_host.data(), c.n_obs_pairs};
     float xd[Plant::N];
-    st.template state_cost<-1>(true, P, ob);   // cart-pole: sin/cos of the current angle
+    st.template state_cost<-1, true>(true, P, ob);   // cart-pole: sin/cos of the current angle
     st.deriv_accurate(u, P, xd);
     st.update(xd, c.dt);
-    const float q = st.template state_cost<-1>(false, P, ob);
+    const float q = st.template state_cost<-1, true>(false, P, ob);
     float xo[16] = {0};
     st.store(xo);
     for (int i = 0; i < c.n; ++i) x[i] = xo[i];

@@ -407,6 +407,20 @@ def test_packed_two_sample_rollout_is_bitwise_scalar():
         assert torch.equal(Ua, Ub)
 
 
+@pytest.mark.parametrize("theta,rate", [(1.2e5, 0.0), (105600.0, 80.0)])
+def test_cartpole_out_of_fast_range_replay_matches_oracle(oracle, theta, rate):
+    """Pole angle beyond the fast sin/cos range (all steps, or crossing it mid-horizon): the
+    one-sample kernel replays such samples with the accurate fallback; costs stay within 1e-4
+    of the fp64 oracle on the well-conditioned samples (at |theta| ~ 1e5 an fp32 angle is only
+    good to 8e-3 rad, so most samples are rightly excluded there) and are finite."""
+    w = get("C1")
+    w.x0 = w.x0.copy()
+    w.x0[2], w.x0[3] = theta, rate
+    costs, ref, key, m, excl, err = _costs_parity(oracle, w, 1024)
+    assert np.isfinite(costs).all()
+    assert excl < 1.0
+
+
 @pytest.mark.parametrize("yaw,rate", [(1.2e5, 0.0), (105600.0, 60.0)])
 def test_packed_out_of_fast_range_replay_is_bitwise_scalar(yaw, rate):
     """Yaw beyond the fast sin/cos range (all steps, or crossing it mid-horizon at different steps
