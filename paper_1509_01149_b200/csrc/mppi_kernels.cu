@@ -217,7 +217,7 @@ __device__ __forceinline__ void eps_ring_loop(const float* eps, size_t row, int 
 
 // One sample's rollout state and its step t for the one-sample kernels.
 // sMat: per-t F_t, G_t of the general path (!DIAG).
-template <class Plant, bool DIAG, int NP>
+template <class Plant, bool DIAG, int NP, bool QSTEP = false>
 struct ScalarRollout {
     static constexpr int M = Plant::M;
     const RolloutArgs<typename Plant::Params>& a;
@@ -291,7 +291,7 @@ struct ScalarRollout {
         }
         st.update(xd, a.dt);
         S += q + is;                                                   // S~ += q~
-        if (a.qstep) {                                                 // q~_{t-1} = q(x_t) + IS_{t-1}
+        if constexpr (QSTEP) {                                         // q~_{t-1} = q(x_t) + IS_{t-1}
             if (!first) a.qstep[(size_t)(t - 1) * a.K_loc + k] = q + is_prev;
             is_prev = is;
         }
@@ -315,7 +315,7 @@ struct ScalarRollout {
     __device__ __forceinline__ float finish() {
         const float qT = st.template state_cost<NP, true>(false, a.P, ob);
         S += qT;
-        if (a.qstep) a.qstep[(size_t)(a.T - 1) * a.K_loc + k] = qT + is_prev;
+        if constexpr (QSTEP) a.qstep[(size_t)(a.T - 1) * a.K_loc + k] = qT + is_prev;
         if (!isfinite(S)) S = a.penalty;
         return S;
     }
@@ -372,7 +372,9 @@ __device__ __forceinline__ void stage_step_constants(const RolloutArgs<PP>& a, f
 template <class Plant>
 constexpr int rollout_min_blocks() { return std::is_same<Plant, Quadrotor>::value ? 4 : 8; }
 
-template <class Plant, bool DIAG, int NP, bool GEN = false>
+// QSTEP: the per-step costs are stored for the cost-to-go weighting (a compile-time switch: a
+// per-step runtime test would split the latency-bound step loop into two basic blocks).
+template <class Plant, bool DIAG, int NP, bool GEN = false, bool QSTEP = false>
 __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
     rollout_kernel(const __grid_constant__ RolloutArgs<typename Plant::Params> a) {
     constexpr int M = Plant::M;
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
             ob.inv_h = a.cell_inv_h;
             ob.band = a.cell_band;
         }
-        ScalarRollout<Plant, DIAG, NP> ro(a, ob, sMat, k);
+        ScalarRollout<Plant, DIAG, NP, QSTEP> ro(a, ob, sMat, k);
         const size_t row = (size_t)a.K_loc * M;
         const StepRec* rec = sRec;
         if constexpr (GEN) {
@@ -1638,11 +1640,21 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     const void* kern;
     if constexpr (X2) {
         kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
-    } else if constexpr (DIAG && (!std::is_same<Plant, Quadrotor>::value || NP == kCellGrid)) {
-        kern = c.gen_eps ? (const void*)rollout_kernel<Plant, DIAG, NP, true> : (const void*)rollout_kernel<Plant, DIAG, NP>;
     } else {
-        if (c.gen_eps) return cudaErrorInvalidValue;   // fused_noise_applies() excludes this variant
-        kern = (const void*)rollout_kernel<Plant, DIAG, NP>;
+        // cost-to-go weighting: the QSTEP variants exist for the runtime-count and grid obstacle
+        // paths (and every other plant); exact-count quadrotor variants defer to NP = -1
+        constexpr bool kQ = NP < 0 || !std::is_same<Plant, Quadrotor>::value;
+        if constexpr (!kQ) {
+            if (c.ctg) return launch_rollout_t<Plant, DIAG, -1>(c, P, x0, U, eps, costs_out);
+        }
+        if constexpr (DIAG && (!std::is_same<Plant, Quadrotor>::value || NP == kCellGrid)) {
+            if (c.ctg) kern = c.gen_eps ? (const void*)rollout_kernel<Plant, DIAG, NP, true, kQ>
+                                        : (const void*)rollout_kernel<Plant, DIAG, NP, false, kQ>;
+            else kern = c.gen_eps ? (const void*)rollout_kernel<Plant, DIAG, NP, true> : (const void*)rollout_kernel<Plant, DIAG, NP>;
+        } else {
+            if (c.gen_eps) return cudaErrorInvalidValue;   // fused_noise_applies() excludes this variant
+            kern = c.ctg ? (const void*)rollout_kernel<Plant, DIAG, NP, false, kQ> : (const void*)rollout_kernel<Plant, DIAG, NP>;
+        }
     }
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
