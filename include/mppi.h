@@ -276,7 +276,7 @@ typedef enum {
                                           among a per-cell candidate list (host-built at create)
                                           instead of all cylinders; bitwise identical results
                                           (default 1) */
-    MPPI_OPTION_BULK_REDUCTION = 5,    /* the weighted-noise reduction streams the noise through a
+    MPPI_OPTION_BULK_REDUCTION = 5,    /* K_loc >= 65536: the weighted-noise reduction streams the noise through a
                                           shared-memory ring filled by bulk copies (cp.async.bulk
                                           + mbarrier) instead of per-thread loads; identical
                                           results (default 1) */

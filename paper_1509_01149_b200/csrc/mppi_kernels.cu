@@ -1306,7 +1306,7 @@ cudaError_t launch_wsum_ctg(Ctx& c, const float* eps) {
     a.cols_per_chunk = c.cols_per_chunk;
     a.neg_inv_lambda = (float)(-1.0 / (double)c.lambda);
     const dim3 grid((unsigned)c.n_chunks, (unsigned)((c.T + kWsumTT - 1) / kWsumTT));
-    if (c.tma_wsum) {
+    if (c.tma_wsum && c.K_loc >= kPackedMinK) {   // small K: plain loads have less latency
         const void* f = c.m == 1 ? (const void*)wsum_ctg_tma_kernel<1> : c.m == 2 ? (const void*)wsum_ctg_tma_kernel<2>
                       : c.m == 4 ? (const void*)wsum_ctg_tma_kernel<4> : nullptr;
         if (!f) return cudaErrorInvalidValue;
@@ -1750,7 +1750,7 @@ cudaError_t launch_wsum(Ctx& c, const float* eps, const long long* key) {
     a.cols_per_chunk = c.cols_per_chunk;
     a.lambda = c.lambda;
     const dim3 grid((unsigned)c.n_chunks, (unsigned)((c.T + kWsumTT - 1) / kWsumTT));
-    if (c.tma_wsum) {
+    if (c.tma_wsum && c.K_loc >= kPackedMinK) {   // small K: plain loads have less latency
         const void* f = c.m == 1 ? (const void*)wsum_tma_kernel<1> : c.m == 2 ? (const void*)wsum_tma_kernel<2>
                       : c.m == 4 ? (const void*)wsum_tma_kernel<4> : nullptr;
         if (!f) return cudaErrorInvalidValue;

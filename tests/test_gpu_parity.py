@@ -489,6 +489,29 @@ def test_pdl_graph_is_bitwise_plain_graph(cfg, K):
     b.close()
 
 
+@pytest.mark.parametrize("cfg,K", [("C4", 65536 + 4), ("C3", 1 << 16), ("C2", (1 << 17) + 8)])
+def test_bulk_copy_reduction_is_bitwise_plain_loads(cfg, K):
+    """MPPI_OPTION_BULK_REDUCTION: the bulk-copy ring and the per-thread-load reduction add the
+    same terms in the same order (m = 4, 2, 1; ragged K), trajectory and cost-to-go weights."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get(cfg)
+    for ctg in (False, True):
+        a = from_workload(w, K=K)
+        b = from_workload(w, K=K)
+        b.set_option(A.MPPI_OPTION_BULK_REDUCTION, 0)
+        if ctg:
+            a.set_weighting(True)
+            b.set_weighting(True)
+        Ua, Ub = cuda_u(w), cuda_u(w)
+        for i in range(2):
+            a.optimize(w.x0, Ua, 2, i)
+            b.optimize(w.x0, Ub, 2, i)
+        torch.cuda.synchronize()
+        assert torch.equal(Ua, Ub) and a.stats() == b.stats()
+        a.close()
+        b.close()
+
+
 @pytest.mark.parametrize("cfg,K,lam", [("C4", 65536, None), ("C4", 65536 + 4, 30.0), ("C4", 1 << 18, 1e4),
                                         ("C3", 16384, 2.0), ("C1", 1000, None)])
 def test_sparse_reduction_is_bitwise_dense(cfg, K, lam):
