@@ -454,7 +454,8 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
 // same packed Box-Muller as K1, so the values are bit-identical to K1's) in step t, and writes
 // them to eps_out for K3; the noise pass and its HBM round trip disappear and the integer/MUFU
 // noise arithmetic interleaves with the FMA-heavy dynamics of the same step.
-template <int NP, bool GEN>
+// QSTEP: per-step costs stored for the cost-to-go weighting (compile-time: 2.4 % at C5).
+template <int NP, bool GEN, bool QSTEP = false>
 __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
     rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
     constexpr int M = 4;
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
             }
             st.update(xd, a.dt);
             S = S + (q + is);                                              // S~ += q~
-            if (a.qstep) {
+            if constexpr (QSTEP) {
                 if (t > 0) *reinterpret_cast<float2*>(a.qstep + (size_t)(t - 1) * a.K_loc + k) = (q + is_prev).v;
                 is_prev = is;
             }
@@ -597,7 +598,7 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
         }
         const V2 qT = st.template state_cost<NP>(false, a.P, ob);         // q(x_T)
         S = S + qT;
-        if (a.qstep) *reinterpret_cast<float2*>(a.qstep + (size_t)(a.T - 1) * a.K_loc + k) = (qT + is_prev).v;
+        if constexpr (QSTEP) *reinterpret_cast<float2*>(a.qstep + (size_t)(a.T - 1) * a.K_loc + k) = (qT + is_prev).v;
         float sa = S.v.x, sb = S.v.y;
         if (!isfinite(sa)) sa = a.penalty;
         if (!isfinite(sb)) sb = a.penalty;
@@ -1639,7 +1640,15 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
                         (NP == kCellGrid ? c.cent_host.size() * sizeof(float2) + c.cells_host.size() * sizeof(uint32_t) : 0);
     const void* kern;
     if constexpr (X2) {
-        kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
+        if (c.ctg) {
+            if constexpr (NP >= 0) {
+                return launch_rollout_t<Plant, DIAG, -1, true>(c, P, x0, U, eps, costs_out);
+            } else {
+                kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true, true> : (const void*)rollout_kernel_x2<NP, false, true>;
+            }
+        } else {
+            kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
+        }
     } else {
         // cost-to-go weighting: the QSTEP variants exist for the runtime-count and grid obstacle
         // paths (and every other plant); exact-count quadrotor variants defer to NP = -1
