@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
                 v[i] = fma2(vb(a.sd[i]), e, vb(uu[i]));                    // U_t + s_i eps_i
                 is = fma2(e, fma2(vb(a.ad[i]), e, vb(bb[i])), is);        // IS_t
             }
-            const V2 q = st.template state_cost<NP>(t == 0, a.P, ob);    // q(x_t): step t-1
+            const V2 q = st.template state_cost<NP, decltype(SAFE)::value>(t == 0, a.P, ob);   // q(x_t): step t-1
             V2 xd[16];
             if constexpr (decltype(SAFE)::value) {
                 if (st.deriv_fast(v, a.P, xd)) st.deriv_accurate(v, a.P, xd);
@@ -579,11 +579,12 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
             body(std::false_type(), t, rec, ea, eb);
             cur = slot_sum - cur;
         }
-        if (__builtin_expect(!(amax <= kSinCosFastMax), 0)) {
-            // An angle left the fast sin/cos range somewhere on this pair's trajectories: replay
-            // both from x0 with the per-step accurate fallback (the inline-fallback semantics),
-            // reading back the noise this pass used.  Never taken on sane trajectories, and
-            // keeping the branch out of the hot loop lets the step body schedule as one block.
+        if (__builtin_expect(!(amax <= kSinCosFastMax) || st.miss, 0)) {
+            // An angle left the fast sin/cos range, or a position left the obstacle grid's band
+            // (or hit an overflow cell), somewhere on this pair's trajectories: replay both from
+            // x0 with the per-step accurate fallbacks (the inline-fallback semantics), reading
+            // back the noise this pass used.  Rare, and keeping the branches out of the hot loop
+            // lets the step body schedule as one block.
             st.load(a.x0_dev ? a.x0_dev : a.x0);
             S = vb(0.0f);
             is_prev = vb(0.0f);
@@ -596,7 +597,7 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
                 body(std::true_type(), t, rec, ea, eb);
             }
         }
-        const V2 qT = st.template state_cost<NP>(false, a.P, ob);         // q(x_T)
+        const V2 qT = st.template state_cost<NP, true>(false, a.P, ob);   // q(x_T)
         S = S + qT;
         if constexpr (QSTEP) *reinterpret_cast<float2*>(a.qstep + (size_t)(a.T - 1) * a.K_loc + k) = (qT + is_prev).v;
         float sa = S.v.x, sb = S.v.y;
