@@ -71,6 +71,6 @@ def build(force=False, verbose=False, out=None, defines=()):
 
 if __name__ == "__main__":
     args = sys.argv[1:]
-    defs = [a for a in args if a.startswith("-D")]
+    defs = [a for a in args if a.startswith("-D")] + [a[len("--flag="):] for a in args if a.startswith("--flag=")]
     outs = [a[len("--out="):] for a in args if a.startswith("--out=")]
     print(build(force=True, verbose="-v" in args, out=outs[0] if outs else None, defines=defs))

@@ -555,6 +555,7 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
             }
         };
         const StepRec* rec = sRec;
+#pragma unroll 2   // two steps per iteration: more scheduling freedom across the step boundary (-1 %)
         for (int t = 0; t < a.T; ++t, ++rec) {
             float ea[4], eb[4];
             if constexpr (GEN) {
