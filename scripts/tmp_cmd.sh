@@ -1,2 +1,5 @@
-timeout 300 python scripts/ab_options.py OBSTACLE_GRID=1
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -rf 2>&1 | tail -3
+for v in "" u2 "" u2; do
+  unset MPPI_LIB
+  if [ -n "$v" ]; then export MPPI_LIB=$PWD/exp/lib_$v.so; fi
+  echo "variant $v"; timeout 300 python scripts/ab_options.py FUSED_NOISE=1
+done
