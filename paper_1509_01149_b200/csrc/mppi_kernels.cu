@@ -1,13 +1,19 @@
 // mppi_kernels.cu — the sm_100a kernels of one MPPI step (Alg. 1, :356-368).
 //
-//   K1 noise_kernel     eps[t][k][0..m) from Philox4x32-10 + BM32        (HBM write / int ALU)
-//   K2 rollout_kernel   one sample per thread, state in registers, T Euler steps accumulating
-//                       S~_k = sum_t q~; block min -> atomicMin key
-//                                                                          (FP32 issue bound)
-//   K3 wsum_kernel      w_k = exp(-(S~_k - S_min)/lambda) and A[t][j] = sum_k w_k eps[t][k][j]:
-//                       the memory-bound K x (T m) GEMV, per-chunk partials  (HBM read bound)
-//   K4 finalize_kernel  fixed-order sum of partials, U_t += sqrt(nu) L A_t / eta
-//   K5 shift_kernel     U_i = U_{i+1}, U_{T-1} = u_init
+//   K1 noise_kernel       eps[t][k][0..m) from Philox4x32-10 + BM32       (HBM write / int ALU)
+//   K2 rollout_kernel     one sample per thread, state in registers, T Euler steps accumulating
+//                         S~_k = sum_t q~; block min -> atomicMin key
+//      rollout_kernel_x2  the quadrotor two samples per thread in packed FP32x2 (the C5 path);
+//                         both can draw eps themselves (GEN: K1's values, written for K3), find
+//                         the nearest cylinder through the candidate grid, and keep the step
+//                         loop one basic block (rare fallbacks replay the sample)   (issue bound)
+//   K3 wsum_tma_kernel    w_k = exp(-(S~_k - S_min)/lambda) and A[t][j] = sum_k w_k eps[t][k][j]:
+//      wsum_kernel        the memory-bound K x (T m) GEMV, per-chunk partials; the tma variant
+//                         streams eps through a bulk-copy ring (K_loc >= 65536) (HBM read bound)
+//   K4 finalize_kernel    fixed-order sum of partials, U_t += sqrt(nu) L A_t / eta
+//   K5 shift_kernel       U_i = U_{i+1}, U_{T-1} = u_init
+//   NEXT rows: ctg_* (cost-to-go weights), advance_kernel (on-device closed loop),
+//   fk_reduce_kernel (Feynman-Kac), general A_t through the !DIAG rollout path.
 //
 // No float atomics anywhere: every reduction has a fixed order, so a step is bitwise
 // reproducible run to run.  The only atomic is an integer atomicMin on the
@@ -21,19 +27,6 @@
 namespace mppi {
 
 // ------------------------------------------------------------------------------ helpers
-template <int M>
-__device__ __forceinline__ void load_eps(const float* p, float* e) {
-    if constexpr (M == 4) {
-        const float4 v = __ldcs(reinterpret_cast<const float4*>(p));
-        e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
-    } else if constexpr (M == 2) {
-        const float2 v = __ldcs(reinterpret_cast<const float2*>(p));
-        e[0] = v.x; e[1] = v.y;
-    } else {
-        e[0] = __ldcs(p);
-    }
-}
-
 template <int M>
 __device__ __forceinline__ void store_eps(float* p, const float* z) {
     if constexpr (M == 4) {
