@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
     // general path: per-t sampling factor F_t and IS matrix G_t after the ring ([T][2][M*M])
     float* sMat = sRing + (GEN ? 0 : kEpsStages * blockDim.x * M);
     // candidate grid (NP == kCellGrid, diagonal path only): centres and cell words
-    float2* sCent = reinterpret_cast<float2*>(sMat);
+    float2* sCent = reinterpret_cast<float2*>(sMat + (DIAG ? 0 : a.T * 2 * M * M));
     uint32_t* sCells = reinterpret_cast<uint32_t*>(sCent + a.n_cent);
     const int tid = threadIdx.x;
     stage_step_constants<M, DIAG>(a, sObs, sRec, sMat);
@@ -1651,7 +1651,7 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
         if constexpr (!kQ) {
             if (c.ctg) return launch_rollout_t<Plant, DIAG, -1>(c, P, x0, U, eps, costs_out);
         }
-        if constexpr (DIAG && (!std::is_same<Plant, Quadrotor>::value || NP == kCellGrid)) {
+        if constexpr (!std::is_same<Plant, Quadrotor>::value || NP == kCellGrid) {
             if (c.ctg) kern = c.gen_eps ? (const void*)rollout_kernel<Plant, DIAG, NP, true, kQ>
                                         : (const void*)rollout_kernel<Plant, DIAG, NP, false, kQ>;
             else kern = c.gen_eps ? (const void*)rollout_kernel<Plant, DIAG, NP, true> : (const void*)rollout_kernel<Plant, DIAG, NP>;
@@ -1699,6 +1699,9 @@ static cudaError_t launch_rollout_np(Ctx& c, const typename Plant::Params& P, co
                                      const float* U, const float* eps, float* costs_out) {
     if constexpr (std::is_same<Plant, Quadrotor>::value && DIAG)
         return dispatch_np<Plant, DIAG, 0>(c, P, x0, U, eps, costs_out);
+    if constexpr (std::is_same<Plant, Quadrotor>::value && !DIAG) {   // general Sigma / A_t
+        if (c.use_cells && c.cell_nx > 0) return launch_rollout_t<Plant, DIAG, kCellGrid>(c, P, x0, U, eps, costs_out);
+    }
     return launch_rollout_t<Plant, DIAG, -1>(c, P, x0, U, eps, costs_out);
 }
 
@@ -1710,12 +1713,14 @@ static cudaError_t launch_rollout_p(Ctx& c, const typename Plant::Params& P, con
 }
 
 bool fused_noise_applies(const Ctx& c) {
-    if (!c.fuse_noise || !c.diag || c.per_t) return false;
-    if (c.plant == MPPI_PLANT_QUADROTOR)   // packed kernel, or the one-sample grid kernel
-        return c.K_loc >= kPackedMinK && (c.pack2 || (c.use_cells && c.cell_nx > 0));
-    // one-sample GEN kernel: only once the step is throughput-bound (measured: -2..4 % at
-    // K = 2^20; at small K the per-thread noise lengthens the latency-bound step loop)
-    return c.K_loc >= kPackedMinK;
+    // GEN kernels only once the step is throughput-bound (measured: -2..4 % at K = 2^20 for the
+    // one-sample kernel; at small K the per-thread noise lengthens the latency-bound step loop)
+    if (!c.fuse_noise || c.K_loc < kPackedMinK) return false;
+    if (c.plant == MPPI_PLANT_QUADROTOR) {
+        if (c.diag && !c.per_t && c.pack2) return true;   // packed kernel (any obstacle path)
+        return c.use_cells && c.cell_nx > 0;               // one-sample grid kernel (any Sigma, A_t)
+    }
+    return true;                                           // one-sample kernel (any Sigma, A_t)
 }
 
 cudaError_t launch_rollout(Ctx& c, const float* x0, const float* U, const float* eps,

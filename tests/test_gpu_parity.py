@@ -537,6 +537,36 @@ def test_sparse_reduction_is_bitwise_dense(cfg, K, lam):
     b.close()
 
 
+@pytest.mark.parametrize("cfg", ["C4", "C3", "C2"])
+def test_general_sigma_fast_paths_are_bitwise(cfg):
+    """Non-diagonal Sigma (the general one-sample path) at K = 65536: drawing the noise in the
+    rollout and (quadrotor) the obstacle grid give the same bits as the separate noise pass and
+    the full search; and the costs stay within tolerance of the oracle."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get(cfg)
+    m = w.m
+    rng = np.random.default_rng(5)
+    B = rng.normal(size=(m, m)) * 0.02
+    Sig = np.array(w.Sigma, dtype=np.float64) + (B @ B.T if m > 1 else 0.0)
+    K = 1 << 16
+    mk = lambda: MPPI(w.plant, K, w.T, w.dt, w.lam, w.nu, Sig, w.R,
+                      obstacles=w.obstacles if w.plant == "quadrotor" else None)
+    a, b = mk(), mk()
+    b.set_option(A.MPPI_OPTION_FUSED_NOISE, 0)
+    if w.plant == "quadrotor":
+        b.set_option(A.MPPI_OPTION_OBSTACLE_GRID, 0)
+    U = cuda_u(w)
+    ca, ka = a.rollout_costs(w.x0, U, 6, 2)
+    cb, kb = b.rollout_costs(w.x0, U, 6, 2)
+    assert torch.equal(ca, cb) and int(ka.item()) == int(kb.item())
+    Ua, Ub = cuda_u(w), cuda_u(w)
+    a.optimize(w.x0, Ua, 6, 2)
+    b.optimize(w.x0, Ub, 6, 2)
+    assert torch.equal(Ua, Ub)
+    a.close()
+    b.close()
+
+
 @pytest.mark.parametrize("xy", [(0.0, 0.0), (25.0, 1.5), (44.0, -9.0), (300.0, 0.0), (-60.0, 80.0), (5000.0, 5.0)])
 def test_obstacle_grid_is_bitwise_full_search(xy):
     """MPPI_OPTION_OBSTACLE_GRID: the per-cell candidate lists give the same nearest-cylinder
