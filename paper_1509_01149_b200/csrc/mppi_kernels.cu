@@ -448,7 +448,10 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
 // them to eps_out for K3; the noise pass and its HBM round trip disappear and the integer/MUFU
 // noise arithmetic interleaves with the FMA-heavy dynamics of the same step.
 // QSTEP: per-step costs stored for the cost-to-go weighting (compile-time: 2.4 % at C5).
-template <int NP, bool GEN, bool QSTEP = false>
+//
+// DIAG = false (correlated Sigma, per-step A_t of NEXT-3): du = F_t eps and the full quadratic
+// IS_t with the per-t matrices staged in shared memory, lane-wise the one-sample kernel's order.
+template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true>
 __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
     rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
     constexpr int M = 4;
@@ -456,33 +459,42 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
     float4* sObs = smem4;
     StepRec* sRec = reinterpret_cast<StepRec*>(smem4 + a.n_obs_pairs);
     float* sRing = reinterpret_cast<float*>(sRec + a.T);               // [2][blockDim][2 samples][4]
-    float2* sCent = reinterpret_cast<float2*>(sRing + (GEN ? 0 : 2 * kRolloutThreads * 2 * 4));
+    float* sMat = sRing + (GEN ? 0 : 2 * kRolloutThreads * 2 * 4);     // !DIAG: [T][2][M*M]
+    float2* sCent = reinterpret_cast<float2*>(sMat + (DIAG ? 0 : a.T * 2 * M * M));
     uint32_t* sCells = reinterpret_cast<uint32_t*>(sCent + a.n_cent);
     const int tid = threadIdx.x;
-    for (int i = tid; i < a.n_obs_pairs; i += blockDim.x) sObs[i] = a.obs[i];
+    // (DIAG keeps its own staging, in this order: the shared helper, or another order, costs
+    // the hot loop 4 % through ptxas' register allocation)
+    if constexpr (DIAG) {
+        for (int i = tid; i < a.n_obs_pairs; i += blockDim.x) sObs[i] = a.obs[i];
+    }
     if constexpr (NP == kCellGrid) {
         for (int i = tid; i < a.n_cent; i += blockDim.x) sCent[i] = a.cent[i];
         const int nc = a.cell_nx * a.cell_ny;
         for (int i = tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
     }
-    for (int t = tid; t < a.T; t += blockDim.x) {
-        float u[4], bq[4];
-        float kk = 0.0f;
+    if constexpr (DIAG) {
+        for (int t = tid; t < a.T; t += blockDim.x) {
+            float u[4], bq[4];
+            float kk = 0.0f;
 #pragma unroll
-        for (int i = 0; i < M; ++i) u[i] = a.U[t * M + i];
+            for (int i = 0; i < M; ++i) u[i] = a.U[t * M + i];
 #pragma unroll
-        for (int i = 0; i < M; ++i) {
-            float ru = 0.0f;
+            for (int i = 0; i < M; ++i) {
+                float ru = 0.0f;
 #pragma unroll
-            for (int j = 0; j < M; ++j) ru = fmaf(a.R[i * M + j], u[j], ru);
-            kk = fmaf(u[i], ru, kk);
-            bq[i] = a.sd[i] * ru;
+                for (int j = 0; j < M; ++j) ru = fmaf(a.R[i * M + j], u[j], ru);
+                kk = fmaf(u[i], ru, kk);
+                bq[i] = a.sd[i] * ru;
+            }
+            StepRec r;
+            r.u = make_float4(u[0], u[1], u[2], u[3]);
+            r.b = make_float4(bq[0], bq[1], bq[2], bq[3]);
+            r.k = make_float4(0.5f * kk, 0.0f, 0.0f, 0.0f);
+            sRec[t] = r;
         }
-        StepRec r;
-        r.u = make_float4(u[0], u[1], u[2], u[3]);
-        r.b = make_float4(bq[0], bq[1], bq[2], bq[3]);
-        r.k = make_float4(0.5f * kk, 0.0f, 0.0f, 0.0f);
-        sRec[t] = r;
+    } else {
+        stage_step_constants<M, DIAG>(a, sObs, sRec, sMat);
     }
     __syncthreads();
     pdl_wait();
@@ -526,11 +538,37 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
             const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
             V2 v[M];
             V2 is = vb(rc->k.x);
+            if constexpr (DIAG) {
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                const V2 e = vp(ea[i], eb[i]);
-                v[i] = fma2(vb(a.sd[i]), e, vb(uu[i]));                    // U_t + s_i eps_i
-                is = fma2(e, fma2(vb(a.ad[i]), e, vb(bb[i])), is);        // IS_t
+                for (int i = 0; i < M; ++i) {
+                    const V2 e = vp(ea[i], eb[i]);
+                    v[i] = fma2(vb(a.sd[i]), e, vb(uu[i]));                    // U_t + s_i eps_i
+                    is = fma2(e, fma2(vb(a.ad[i]), e, vb(bb[i])), is);        // IS_t
+                }
+            } else {
+                // du = F_t eps, IS_t = du'G_t du + (R U_t).du + K_t (as ScalarRollout, lane-wise).
+                // F_t is addressed from the shared-memory base, not a captured pointer: the DIAG
+                // instantiation must not carry one more live value through the loop
+                const float* F = reinterpret_cast<const float*>(smem4 + a.n_obs_pairs) + a.T * (sizeof(StepRec) / 4) +
+                                 (GEN ? 0 : 2 * kRolloutThreads * 2 * 4) + t * 2 * M * M;
+                const float* G = F + M * M;
+                V2 du[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    V2 d = vb(0.0f);
+#pragma unroll
+                    for (int j = 0; j < M; ++j) d = fma2(vb(F[i * M + j]), vp(ea[j], eb[j]), d);
+                    du[i] = d;
+                    v[i] = vb(uu[i]) + d;
+                }
+                V2 duGdu = vb(0.0f), uRdu = vb(0.0f);
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+#pragma unroll
+                    for (int j = 0; j < M; ++j) duGdu = fma2(du[i] * vb(G[i * M + j]), du[j], duGdu);
+                    uRdu = fma2(vb(bb[i]), du[i], uRdu);
+                }
+                is = duGdu + (uRdu + is);
             }
             const V2 q = st.template state_cost<NP, decltype(SAFE)::value>(t == 0, a.P, ob);   // q(x_t): step t-1
             V2 xd[16];
@@ -1634,7 +1672,11 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
                         (DIAG ? 0 : (size_t)c.T * 2 * Plant::M * Plant::M * sizeof(float)) +
                         (NP == kCellGrid ? c.cent_host.size() * sizeof(float2) + c.cells_host.size() * sizeof(uint32_t) : 0);
     const void* kern;
-    if constexpr (X2) {
+    if constexpr (X2 && !DIAG) {   // general Sigma / A_t: grid path only
+        static_assert(NP == kCellGrid, "packed general-Sigma kernel: candidate-grid path only");
+        if (c.ctg) kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true, true, false> : (const void*)rollout_kernel_x2<NP, false, true, false>;
+        else kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true, false, false> : (const void*)rollout_kernel_x2<NP, false, false, false>;
+    } else if constexpr (X2) {
         if (c.ctg) {
             if constexpr (NP >= 0) {
                 return launch_rollout_t<Plant, DIAG, -1, true>(c, P, x0, U, eps, costs_out);
@@ -1700,7 +1742,11 @@ static cudaError_t launch_rollout_np(Ctx& c, const typename Plant::Params& P, co
     if constexpr (std::is_same<Plant, Quadrotor>::value && DIAG)
         return dispatch_np<Plant, DIAG, 0>(c, P, x0, U, eps, costs_out);
     if constexpr (std::is_same<Plant, Quadrotor>::value && !DIAG) {   // general Sigma / A_t
-        if (c.use_cells && c.cell_nx > 0) return launch_rollout_t<Plant, DIAG, kCellGrid>(c, P, x0, U, eps, costs_out);
+        if (c.use_cells && c.cell_nx > 0) {
+            if (c.pack2 && c.K_loc >= kPackedMinK)
+                return launch_rollout_t<Plant, DIAG, kCellGrid, true>(c, P, x0, U, eps, costs_out);
+            return launch_rollout_t<Plant, DIAG, kCellGrid>(c, P, x0, U, eps, costs_out);
+        }
     }
     return launch_rollout_t<Plant, DIAG, -1>(c, P, x0, U, eps, costs_out);
 }

@@ -555,16 +555,24 @@ def test_general_sigma_fast_paths_are_bitwise(cfg):
     b.set_option(A.MPPI_OPTION_FUSED_NOISE, 0)
     if w.plant == "quadrotor":
         b.set_option(A.MPPI_OPTION_OBSTACLE_GRID, 0)
+    variants = [b]
+    if w.plant == "quadrotor":                      # packed general-Sigma kernel vs one-sample
+        c = mk()
+        c.set_option(A.MPPI_OPTION_PACKED_SAMPLES, 0)
+        variants.append(c)
     U = cuda_u(w)
     ca, ka = a.rollout_costs(w.x0, U, 6, 2)
-    cb, kb = b.rollout_costs(w.x0, U, 6, 2)
-    assert torch.equal(ca, cb) and int(ka.item()) == int(kb.item())
-    Ua, Ub = cuda_u(w), cuda_u(w)
+    for v in variants:
+        cb, kb = v.rollout_costs(w.x0, U, 6, 2)
+        assert torch.equal(ca, cb) and int(ka.item()) == int(kb.item())
+    Ua = cuda_u(w)
     a.optimize(w.x0, Ua, 6, 2)
-    b.optimize(w.x0, Ub, 6, 2)
-    assert torch.equal(Ua, Ub)
+    for v in variants:
+        Ub = cuda_u(w)
+        v.optimize(w.x0, Ub, 6, 2)
+        assert torch.equal(Ua, Ub)
+        v.close()
     a.close()
-    b.close()
 
 
 @pytest.mark.parametrize("xy", [(0.0, 0.0), (25.0, 1.5), (44.0, -9.0), (300.0, 0.0), (-60.0, 80.0), (5000.0, 5.0)])
