@@ -30,7 +30,7 @@ UNIT = "K*T/s"
 # FP32 FLOPs per sample-step of the rollout kernel (FADD + FMUL + 2 FFMA + 2 FADD2 + 2 FMUL2 +
 # 4 FFMA2 per thread, ncu sass counters / (K*T)); see DESIGN.md "Rollout FLOPs".  None -> not
 # yet measured for that plant (roofline falls back to the kernel's measured share only).
-ROLLOUT_FLOP_PER_SS = {"cartpole": 59.43, "racecar": 251.49,  # profiles/r1_rollout_flops_*_v7.csv
+ROLLOUT_FLOP_PER_SS = {"cartpole": 59.43, "racecar": 249.6,   # profiles/r1_rollout_flops_*_v13.csv
                        "quadrotor": 464.56}  # profiles/r1_ncu_full_c5_v7.txt (rollout v7, x2)
 # The packed quadrotor rollout with the obstacle candidate grid and the in-kernel noise (the C5
 # path, K_loc >= 65536): FP32 FLOPs, issued thread instructions and DRAM bytes per sample-step,
