@@ -34,10 +34,10 @@ ROLLOUT_FLOP_PER_SS = {"cartpole": 59.43, "racecar": 249.6,   # profiles/r1_roll
                        "quadrotor": 464.56}  # profiles/r1_ncu_full_c5_v7.txt (rollout v7, x2)
 # The packed quadrotor rollout with the obstacle candidate grid and the in-kernel noise (the C5
 # path, K_loc >= 65536): FP32 FLOPs, issued thread instructions and DRAM bytes per sample-step,
-# ncu --set full at C5 (profiles/r1_ncu_full_c5_v12.txt).  The kernel also draws the noise
+# ncu --set full at C5 (profiles/r1_ncu_full_c5_v13.txt).  The kernel also draws the noise
 # (Philox integer work, Box-Muller) so it is issue-bound on a mixed integer/FP32 stream; the
 # FP32-pipe fraction is the roofline, the issue-slot fraction is reported beside it.
-FUSED_QUAD = {"flop": 357.60, "inst": 312.53, "dram_bytes": 15.953}
+FUSED_QUAD = {"flop": 358.10, "inst": 311.85, "dram_bytes": 15.953}
 
 
 def rollout_variant(w, K_loc):
