@@ -173,6 +173,9 @@ cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* 
 cudaError_t launch_shift(Ctx& c, float* U, const float* u_init);
 int wsum_blocks_per_sm(int m);  // resident wsum CTAs per SM (occupancy API)
 bool fused_noise_applies(const Ctx& c);  // the rollout kernel for c can draw its own noise
+size_t rollout_smem_bytes(const Ctx& c, bool cells);   // dynamic smem of the rollout kernels
+size_t smem_optin_bytes();                             // the device's per-block opt-in limit
+bool grid_on(const Ctx& c);              // the obstacle candidate grid is in use
 // NCCL (mppi_nccl.cu): runtime-resolved, 0 on success, >0 ncclResult_t, -1 unavailable
 bool nccl_available();
 int nccl_unique_id(unsigned char* out);

@@ -1718,7 +1718,7 @@ template <class Plant, bool DIAG, int NP>
 static cudaError_t dispatch_np(Ctx& c, const typename Plant::Params& P, const float* x0,
                                const float* U, const float* eps, float* costs_out) {
     if constexpr (NP == 0) {
-        if (c.use_cells && c.cell_nx > 0) {
+        if (grid_on(c)) {
             if (c.pack2 && c.K_loc >= kPackedMinK)
                 return launch_rollout_t<Plant, DIAG, kCellGrid, true>(c, P, x0, U, eps, costs_out);
             return launch_rollout_t<Plant, DIAG, kCellGrid>(c, P, x0, U, eps, costs_out);
@@ -1742,7 +1742,7 @@ static cudaError_t launch_rollout_np(Ctx& c, const typename Plant::Params& P, co
     if constexpr (std::is_same<Plant, Quadrotor>::value && DIAG)
         return dispatch_np<Plant, DIAG, 0>(c, P, x0, U, eps, costs_out);
     if constexpr (std::is_same<Plant, Quadrotor>::value && !DIAG) {   // general Sigma / A_t
-        if (c.use_cells && c.cell_nx > 0) {
+        if (grid_on(c)) {
             if (c.pack2 && c.K_loc >= kPackedMinK)
                 return launch_rollout_t<Plant, DIAG, kCellGrid, true>(c, P, x0, U, eps, costs_out);
             return launch_rollout_t<Plant, DIAG, kCellGrid>(c, P, x0, U, eps, costs_out);
@@ -1758,13 +1758,40 @@ static cudaError_t launch_rollout_p(Ctx& c, const typename Plant::Params& P, con
                   : launch_rollout_np<Plant, false>(c, P, x0, U, eps, costs_out);
 }
 
+// Dynamic shared memory of the rollout kernels (obstacle pairs, per-t records, the eps ring,
+// the general path's per-t matrices, the candidate grid), and the device's opt-in limit.
+size_t rollout_smem_bytes(const Ctx& c, bool cells) {
+    const int m = c.m;
+    return (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
+           (size_t)kEpsStages * kRolloutThreads * m * sizeof(float) +
+           (c.diag ? 0 : (size_t)c.T * 2 * m * m * sizeof(float)) +
+           (cells ? c.cent_host.size() * sizeof(float2) + c.cells_host.size() * sizeof(uint32_t) : 0);
+}
+
+size_t smem_optin_bytes() {
+    static size_t v = [] {
+        int dev = 0, b = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&b, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || b <= 0)
+            b = 227 * 1024;
+        return (size_t)b;
+    }();
+    return v;
+}
+
+// the obstacle candidate grid is used when it was built, is enabled and fits in shared memory
+// beside the horizon's per-t records (very long horizons fall back to the full search)
+bool grid_on(const Ctx& c) {
+    return c.use_cells && c.cell_nx > 0 && rollout_smem_bytes(c, true) <= smem_optin_bytes();
+}
+
 bool fused_noise_applies(const Ctx& c) {
     // GEN kernels only once the step is throughput-bound (measured: -2..4 % at K = 2^20 for the
     // one-sample kernel; at small K the per-thread noise lengthens the latency-bound step loop)
     if (!c.fuse_noise || c.K_loc < kPackedMinK) return false;
     if (c.plant == MPPI_PLANT_QUADROTOR) {
         if (c.diag && !c.per_t && c.pack2) return true;   // packed kernel (any obstacle path)
-        return c.use_cells && c.cell_nx > 0;               // one-sample grid kernel (any Sigma, A_t)
+        return grid_on(c);                                 // one-sample grid kernel (any Sigma, A_t)
     }
     return true;                                           // one-sample kernel (any Sigma, A_t)
 }

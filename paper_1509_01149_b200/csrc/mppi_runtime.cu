@@ -470,6 +470,12 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
 
     cudaError_t e = cudaGetDevice(&c.device);
     if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaGetDevice (no CUDA device?)"); }
+    if (rollout_smem_bytes(c, false) > smem_optin_bytes()) {
+        const size_t need = rollout_smem_bytes(c, false);
+        delete ctx;
+        return fail(MPPI_ERR_INVALID_ARG, "T = %d needs %zu B of shared memory per rollout CTA (limit %zu)", T,
+                    need, smem_optin_bytes());
+    }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
     // weighted-noise reduction grid (n_chunks x t-tiles CTAs): a whole number of waves of the
@@ -832,8 +838,14 @@ mppi_status_t mppi_set_sampling_transform(mppi_ctx* ctx, const double* A) {
         if (mppi_status_t a = dalloc(c, &c.d_mats, (size_t)c.T * 32, "sampling transforms")) return a;
     }
     MPPI_CUDA(cudaMemcpy(c.d_mats, mats.data(), mats.size() * sizeof(float), cudaMemcpyHostToDevice), "A_t upload");
-    c.per_t = true;
+    const bool diag_before = c.diag;
     c.diag = false;
+    if (rollout_smem_bytes(c, false) > smem_optin_bytes()) {
+        c.diag = diag_before;
+        return fail(MPPI_ERR_INVALID_ARG, "per-step transforms at T = %d need %zu B of shared memory per rollout CTA",
+                    c.T, rollout_smem_bytes(c, false));
+    }
+    c.per_t = true;
     return MPPI_OK;
 }
 

@@ -19,7 +19,7 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
 from mppi_inputs import get  # noqa: E402
-from paper_1509_01149_b200 import MPPI, from_workload  # noqa: E402
+from paper_1509_01149_b200 import MPPI, MppiError, from_workload  # noqa: E402
 
 COST_RTOL = 1e-4
 U_ATOL = 1e-5
@@ -573,6 +573,29 @@ def test_general_sigma_fast_paths_are_bitwise(cfg):
         assert torch.equal(Ua, Ub)
         v.close()
     a.close()
+
+
+def test_longest_horizon():
+    """T = 4096 (the ABI maximum): the obstacle grid no longer fits in shared memory beside the
+    per-step records, so the quadrotor falls back to the full search; packed and one-sample
+    kernels still agree bit for bit.  A correlated Sigma at that horizon (per-step matrices do
+    not fit) is refused at create."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get("C4", T=4096)
+    a = from_workload(w, K=1 << 16)
+    b = from_workload(w, K=1 << 16)
+    b.set_option(A.MPPI_OPTION_PACKED_SAMPLES, 0)
+    U = cuda_u(w)
+    ca, ka = a.rollout_costs(w.x0, U, 1, 0)
+    cb, kb = b.rollout_costs(w.x0, U, 1, 0)
+    assert torch.isfinite(ca).all() and torch.equal(ca, cb) and int(ka.item()) == int(kb.item())
+    a.optimize(w.x0, U, 1, 0)
+    assert torch.isfinite(U).all()
+    a.close()
+    b.close()
+    Sig = np.array(w.Sigma, np.float64) + 1e-4
+    with pytest.raises(MppiError):
+        MPPI(w.plant, 1 << 16, 4096, w.dt, w.lam, w.nu, Sig, w.R, obstacles=w.obstacles)
 
 
 @pytest.mark.parametrize("xy", [(0.0, 0.0), (25.0, 1.5), (44.0, -9.0), (300.0, 0.0), (-60.0, 80.0), (5000.0, 5.0)])
