@@ -208,7 +208,9 @@ typedef struct {
  *   dynamics, cost : HOST structs, copied (obstacles too).  cost->penalty must be finite.
  *   K              : global number of samples, >= 1; K_loc = K/world must be an integer
  *                    multiple of 4 (16-byte aligned noise rows).
- *   T              : horizon steps, 1..4096.
+ *   T              : horizon steps, 1..4096 (a non-diagonal Sigma or R keeps two m x m matrices
+ *                    per step in shared memory: INVALID_ARG when they no longer fit, T > ~1200
+ *                    at m = 4).
  *   dt             : Euler step > 0.
  *   lambda         : temperature > 0.
  *   nu             : exploration variance scale >= 1 (PAPER.md:308; Gamma invertible, :197).
