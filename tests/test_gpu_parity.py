@@ -230,12 +230,13 @@ def test_determinism():
         assert torch.equal(c, outs[0][0]) and torch.equal(U, outs[0][1]) and k == outs[0][2]
 
 
-@pytest.mark.parametrize("K", [8192, 1 << 19])
+@pytest.mark.parametrize("K", [8192, 1 << 19, 1 << 22])
 def test_sharded_split_phase_matches_single_gpu(K):
     """P13 emulated on one GPU (SURVEY §4 "fake backend"): G = 2, 4, 8 contexts with rank/world
     run their shards; the host combines MIN of keys and SUM of [eta, A]; noise, costs and k* are
     bitwise the single-GPU ones and U agrees within 1e-6.  K = 2^19 puts every shard of G <= 8 on
-    the packed kernels with in-kernel noise (K_loc >= 65536)."""
+    the packed kernels with in-kernel noise (K_loc >= 65536); K = 2^22 is C5, the bench's
+    strong-scaling workload (its G = 8 shards are the per-GPU work of the 8-GPU run)."""
     w = get("C4")
     single = from_workload(w, K=K)
     U1 = cuda_u(w)
