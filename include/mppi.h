@@ -437,6 +437,18 @@ mppi_status_t mppi_noise(mppi_ctx* ctx, uint64_t seed, uint64_t step, float* out
 mppi_status_t mppi_plant_step(mppi_ctx* ctx, float* x, const float* u, int32_t* crashed,
                               float* q_out);
 
+/* mppi_obstacle_grid — HOST only (no device, no context): the nearest-cylinder candidate grid
+ * mppi_create builds for the quadrotor, for inspection and tests.
+ *   xy     : HOST float [n][2] cylinder centres, 2 <= n <= 127 (else UNSUPPORTED: no grid).
+ *   words  : HOST uint32 [capacity] or NULL; receives the [ny][nx] cell words (four 7-bit centre
+ *            indices, unused slots repeating the first, 3-bit count in bits 28..30, 0 = no list).
+ *   geom   : HOST float [6] = (nx, ny, ox, oy, inv_h, band): a point p lies in cell
+ *            (floor(p.x * inv_h + ox), floor(p.y * inv_h + oy)) (fp32 fma), border cells
+ *            extending `band` cells outward.
+ * Errors: INVALID_ARG (NULL xy / geom, capacity < nx * ny with words != NULL), UNSUPPORTED. */
+mppi_status_t mppi_obstacle_grid(const float* xy, int32_t n, uint32_t* words, int64_t capacity,
+                                 float* geom);
+
 /* mppi_get_stats — SYNCHRONOUS: waits for the stream, then reads the last step's k*, S_min
  * and eta (eta is this rank's local sum unless mppi_apply ran with a summed buffer). */
 mppi_status_t mppi_get_stats(mppi_ctx* ctx, mppi_stats_t* out /* HOST */);

@@ -103,7 +103,8 @@ KERNEL_NAMES = ["noise", "rollout", "wsum", "finalize", "shift"]
 EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize", "mppi_use_graph", "mppi_set_option",
            "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_apply",
            "mppi_shift", "mppi_noise", "mppi_feynman_kac", "mppi_closed_loop", "mppi_set_weighting",
-           "mppi_cost_to_go", "mppi_set_sampling_transform", "mppi_nccl_unique_id", "mppi_nccl_attach", "mppi_plant_step", "mppi_get_stats",
+           "mppi_cost_to_go", "mppi_set_sampling_transform", "mppi_nccl_unique_id", "mppi_nccl_attach",
+           "mppi_obstacle_grid", "mppi_plant_step", "mppi_get_stats",
            "mppi_last_launch_count", "mppi_profile_enable", "mppi_profile_read", "mppi_last_error", "mppi_status_string", "mppi_abi_version"]
 
 _lib = None
@@ -147,6 +148,9 @@ def lib():
     L.mppi_apply.restype = st
     L.mppi_shift.argtypes = [vp, vp, fp]
     L.mppi_shift.restype = st
+    L.mppi_obstacle_grid.argtypes = [C.POINTER(C.c_float), C.c_int32, C.POINTER(C.c_uint32), C.c_int64,
+                                     C.POINTER(C.c_float)]
+    L.mppi_obstacle_grid.restype = st
     L.mppi_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
     L.mppi_nccl_unique_id.restype = st
     L.mppi_nccl_attach.argtypes = [vp, C.POINTER(C.c_uint8)]

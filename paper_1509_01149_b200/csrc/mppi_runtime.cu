@@ -944,6 +944,26 @@ mppi_status_t mppi_plant_step(mppi_ctx* ctx, float* x, const float* u, int32_t* 
     return MPPI_OK;
 }
 
+mppi_status_t mppi_obstacle_grid(const float* xy, int32_t n, uint32_t* words, int64_t capacity, float* geom) {
+    if (!xy || !geom) return fail(MPPI_ERR_INVALID_ARG, "xy and geom must be non-NULL");
+    if (n < 2 || n > (1 << kCellIdxBits)) return fail(MPPI_ERR_UNSUPPORTED, "no grid for %d obstacles", n);
+    if (!all_finite(xy, 2 * n)) return fail(MPPI_ERR_INVALID_ARG, "obstacle centres must be finite");
+    Ctx c;
+    build_cell_grid(c, xy, n);
+    if (c.cell_nx == 0) return fail(MPPI_ERR_UNSUPPORTED, "degenerate obstacle layout: no grid");
+    geom[0] = (float)c.cell_nx;
+    geom[1] = (float)c.cell_ny;
+    geom[2] = c.cell_ox;
+    geom[3] = c.cell_oy;
+    geom[4] = c.cell_inv_h;
+    geom[5] = c.cell_band;
+    if (words) {
+        if (capacity < (int64_t)c.cells_host.size()) return fail(MPPI_ERR_INVALID_ARG, "capacity below nx * ny");
+        memcpy(words, c.cells_host.data(), c.cells_host.size() * sizeof(uint32_t));
+    }
+    return MPPI_OK;
+}
+
 mppi_status_t mppi_get_stats(mppi_ctx* ctx, mppi_stats_t* out) {
     if (mppi_status_t s = check_ctx(ctx)) return s;
     if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
