@@ -266,30 +266,34 @@ mppi_status_t mppi_use_graph(mppi_ctx* ctx, int32_t enable);
 
 typedef enum {
     MPPI_OPTION_CUDA_GRAPH = 1,        /* same as mppi_use_graph (default 1) */
-    MPPI_OPTION_PACKED_SAMPLES = 2,    /* quadrotor, diagonal Sigma and R, K_loc >= 65536: two samples
-                                          per thread with FP32x2 arithmetic (default 1); bitwise
+    MPPI_OPTION_PACKED_SAMPLES = 2,    /* quadrotor, K_loc >= 65536: two samples per thread with FP32x2
+                                          arithmetic (diagonal or general Sigma / A_t; the general
+                                          variant needs the obstacle grid) (default 1); bitwise
                                           identical results */
-    MPPI_OPTION_FUSED_NOISE = 3,       /* when the library draws the noise, diagonal Sigma and R and
-                                          K_loc >= 65536: the rollout kernel draws it itself (same
-                                          counters, bit-identical values, still written to the
-                                          context's noise buffer for the reduction) instead of a
-                                          separate noise pass (default 1) */
-    MPPI_OPTION_OBSTACLE_GRID = 4,     /* packed quadrotor rollout: the nearest cylinder is searched
-                                          among a per-cell candidate list (host-built at create)
-                                          instead of all cylinders; bitwise identical results
+    MPPI_OPTION_FUSED_NOISE = 3,       /* when the library draws the noise and K_loc >= 65536: the
+                                          rollout kernel draws it itself (same counters,
+                                          bit-identical values, still written to the context's noise
+                                          buffer for the reduction) instead of a separate noise
+                                          pass (default 1) */
+    MPPI_OPTION_OBSTACLE_GRID = 4,     /* quadrotor: the nearest cylinder is searched among a per-cell
+                                          candidate list (host-built at create, see
+                                          mppi_obstacle_grid) instead of all cylinders, when the
+                                          grid fits in shared memory beside the horizon's per-step
+                                          records; bitwise identical results (default 1) */
+    MPPI_OPTION_BULK_REDUCTION = 5,    /* K_loc >= 65536: the weighted-noise reductions (trajectory and
+                                          cost-to-go weights) stream their tiles through a shared-
+                                          memory ring filled by bulk copies (cp.async.bulk +
+                                          mbarrier) instead of per-thread loads; identical results
                                           (default 1) */
-    MPPI_OPTION_BULK_REDUCTION = 5,    /* K_loc >= 65536: the weighted-noise reduction streams the noise through a
-                                          shared-memory ring filled by bulk copies (cp.async.bulk
-                                          + mbarrier) instead of per-thread loads; identical
-                                          results (default 1) */
     MPPI_OPTION_PDL = 6,               /* the step's CUDA graph links its kernels with programmatic
                                           (dependent-launch) edges: a kernel's CTAs launch as the
                                           previous kernel's last CTAs exit and wait
                                           (griddepcontrol.wait) for its results; identical results.
                                           Default 0: on B200 it saves ~1.5 us of p50 latency at
                                           C1-C3 but adds ~10 us to the C1 p99 */
-    MPPI_OPTION_SPARSE_REDUCTION = 7   /* with the bulk-copy reduction and K_loc >= 65536: a pass over the costs flags the
-                                          256-column blocks holding a nonzero fp32 weight and the
+    MPPI_OPTION_SPARSE_REDUCTION = 7   /* with the bulk-copy reduction (K_loc >= 65536, trajectory
+                                          weights): a pass over the costs flags the 256-column
+                                          blocks holding a nonzero fp32 weight and the
                                           weighted noise sum streams only those (zero weights add
                                           exact zeros: identical results).  With small lambda the
                                           weights are nearly one-hot (C1-C5: one nonzero weight), and
