@@ -38,12 +38,18 @@ ROLLOUT_FLOP_PER_SS = {"cartpole": 59.43, "racecar": 249.6,   # profiles/r1_roll
 # (Philox integer work, Box-Muller) so it is issue-bound on a mixed integer/FP32 stream; the
 # FP32-pipe fraction is the roofline, the issue-slot fraction is reported beside it.
 FUSED_QUAD = {"flop": 358.10, "inst": 311.85, "dram_bytes": 15.953}
+# The same kernel with the fused reduction epilogue (MPPI_OPTION_FUSED_REDUCTION, the default):
+# each CTA also forms its samples' weights and weighted noise sums, re-reading the noise it wrote
+# (profiles/r1_ncu_full_c5_v14.txt).  Algorithmic bytes: the noise written and read back once,
+# 2 * 4 m per sample-step.
+FUSED_QUAD_EPI = {"flop": 366.99, "inst": 328.17, "dram_bytes": 32.07}
 
 
-def rollout_variant(w, K_loc):
-    """Which rollout kernel bench.py's configuration runs (mirrors dispatch_np/fused_noise_applies)."""
+def rollout_variant(w, K_loc, fused_reduction=True):
+    """Which rollout kernel bench.py's configuration runs (mirrors dispatch_np/fused_noise_applies/
+    epi_applies)."""
     if w.plant == "quadrotor" and K_loc >= 65536 and w.obstacles is not None and len(w.obstacles) >= 2:
-        return "x2-grid-fused"
+        return "x2-grid-fused-epi" if fused_reduction else "x2-grid-fused"
     return "scalar"
 
 SM_COUNT_B200 = 148
@@ -285,7 +291,8 @@ def _safe(fn, *a, **k):
 
 
 # ----------------------------------------------------------------------------- other configs
-def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=False):
+def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=False,
+               fused_reduction=True, profile=False):
     """K*T/s of one config on this GPU (graph replay, CUDA events around `steps` steps)."""
     import torch
     from mppi_inputs import get
@@ -294,8 +301,11 @@ def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=Fals
     m = from_workload(w, K=K or w.K)
     if cost_to_go:
         m.set_weighting(True)
-    if sparse:
+    if sparse:      # the sparse skip belongs to the separate K3 reduction
+        m.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
         m.set_option(A.MPPI_OPTION_SPARSE_REDUCTION, 1)
+    if not fused_reduction:
+        m.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
     U = torch.tensor(w.U0, device="cuda")
     for i in range(warm):
         m.optimize(w.x0, U, w.seed, i)
@@ -307,11 +317,27 @@ def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=Fals
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
+    kern = None
+    if profile:     # a separate profiled pass (per-kernel CUDA events), after the timed one
+        m.profile_enable(True)
+        for i in range(steps):
+            m.optimize(w.x0, U, w.seed, warm + steps + i)
+        kt = m.profile_read()
+        m.profile_enable(False)
+        kern = {k: v[0] / v[1] for k, v in kt.items() if v[1]}
+        if not fused_reduction and kern.get("wsum"):
+            b = 4.0 * w.T * (K or w.K) * w.m + 4.0 * (K or w.K)
+            pk = measured_peaks()
+            kern["wsum_hbm_GBps"] = b / (kern["wsum"] * 1e-3) / 1e9
+            kern["wsum_hbm_frac"] = kern["wsum_hbm_GBps"] / pk.get("hbm_gbs", 6650.0)
     m.close()
-    return {"plant": w.plant, "K": K or w.K, "T": w.T, "ms_per_step": ms,
+    return {"plant": w.plant, "K": K or w.K, "T": w.T, "ms_per_step": ms, "kernel_avg_ms": kern,
             "KT_per_s": (K or w.K) * w.T / (ms * 1e-3),
             "weighting": "cost-to-go (PAPER.md:320-322)" if cost_to_go else "trajectory",
-            "reduction": "sparse (all-zero weight blocks skipped, bit-identical)" if sparse else "dense GEMV"}
+            "rollout": rollout_variant(w, K or w.K, fused_reduction and not sparse),
+            "reduction": ("sparse (all-zero weight blocks skipped, bit-identical)" if sparse else
+                          "fused into the rollout" if rollout_variant(w, K or w.K, fused_reduction)
+                          .endswith("-epi") else "dense GEMV")}
 
 
 def c_abi_closed_loop(steps=200):
@@ -547,21 +573,24 @@ def main():
     avg_s = kern[dom]["avg_ms"] * 1e-3
     K_loc = K // world
     roof = {"kernel": dom}
+    variant_of_step = rollout_variant(w, K_loc)
     if dom == "rollout":
         fp = fp32_peak(probe, props.multi_processor_count, sm_max)
         variant = rollout_variant(w, K_loc)
-        fused = variant == "x2-grid-fused"
-        fl = FUSED_QUAD["flop"] if fused else ROLLOUT_FLOP_PER_SS.get(w.plant)
+        fused = variant.startswith("x2-grid-fused")
+        fq = FUSED_QUAD_EPI if variant.endswith("-epi") else FUSED_QUAD
+        fl = fq["flop"] if fused else ROLLOUT_FLOP_PER_SS.get(w.plant)
         units = K_loc * w.T
         ach = fl * units / avg_s / 1e12 if fl else None
         roof.update({"bound": "alu", "achieved": ach, "peak": fp["peak_tflops"], "unit": "TFLOP/s",
                      "frac": ach / fp["peak_tflops"] if ach else None,
-                     "traffic": FUSED_QUAD["dram_bytes"] * units if fused else None,
-                     "algorithmic_bytes_per_launch": 4.0 * w.m * units + 4.0 * K_loc if fused else None,
+                     "traffic": fq["dram_bytes"] * units if fused else None,
+                     "algorithmic_bytes_per_launch": ((8.0 if variant.endswith("-epi") else 4.0) * w.m * units
+                                                      + 4.0 * K_loc) if fused else None,
                      "flop_per_sample_step": fl, "variant": variant, "peak_detail": fp})
         if fused:   # issue-slot utilisation: 1 warp instruction / cycle / SM sub-partition
             slots = props.multi_processor_count * 4 * sm_max * 1e6
-            roof["issue_frac"] = FUSED_QUAD["inst"] / 32.0 * units / avg_s / slots
+            roof["issue_frac"] = fq["inst"] / 32.0 * units / avg_s / slots
             # the FP32 work of the same step done the direct way (full 50-cylinder search, noise
             # read from HBM: the v7 kernel's ncu count) over this kernel's time -- an effective
             # rate, not executed FLOPs
@@ -577,7 +606,9 @@ def main():
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"})
     # secondary rooflines: the HBM-bound reduction and noise kernels
     extra = {}
-    if kern["wsum"]["avg_ms"]:
+    if variant_of_step.endswith("-epi"):
+        extra["epi_combine_ms"] = kern["wsum"]["avg_ms"]   # K3 is the per-CTA partial combine
+    elif kern["wsum"]["avg_ms"]:
         b = 4.0 * w.T * K_loc * w.m + 4.0 * K_loc
         extra["wsum_hbm_GBps"] = b / (kern["wsum"]["avg_ms"] * 1e-3) / 1e9
         extra["wsum_hbm_frac"] = extra["wsum_hbm_GBps"] / pk.get("hbm_gbs", 6650.0)
@@ -604,6 +635,8 @@ def main():
                  "C5_sweep": [throughput("C5", K=1 << e, steps=5) for e in (16, 18, 20, 22)],
                  "C5_cost_to_go": throughput("C5", steps=5, cost_to_go=True),
                  "C5_sparse_reduction": throughput("C5", steps=5, sparse=True),
+                 "C5_separate_reduction": _safe(throughput, "C5", steps=5, fused_reduction=False,
+                                                profile=True),
                  "c_abi_closed_loop": _safe(c_abi_closed_loop),
                  "closed_loop": closed_loop("C2"),
                  "device_closed_loop": device_closed_loop("C2"),

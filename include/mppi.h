@@ -291,7 +291,7 @@ typedef enum {
                                           (griddepcontrol.wait) for its results; identical results.
                                           Default 0: on B200 it saves ~1.5 us of p50 latency at
                                           C1-C3 but adds ~10 us to the C1 p99 */
-    MPPI_OPTION_SPARSE_REDUCTION = 7   /* with the bulk-copy reduction (K_loc >= 65536, trajectory
+    MPPI_OPTION_SPARSE_REDUCTION = 7,  /* with the bulk-copy reduction (K_loc >= 65536, trajectory
                                           weights): a pass over the costs flags the 256-column
                                           blocks holding a nonzero fp32 weight and the
                                           weighted noise sum streams only those (zero weights add
@@ -300,6 +300,14 @@ typedef enum {
                                           the reduction then reads kilobytes instead of 4 T K m bytes.
                                           Default 0: bench.py measures the dense GEMV the north_star
                                           defines and reports this mode beside it */
+    MPPI_OPTION_FUSED_REDUCTION = 8    /* packed quadrotor path (diagonal Sigma and R, obstacle grid,
+                                          in-kernel noise, trajectory weights): every rollout CTA
+                                          weights its samples against its own minimum and forms its
+                                          partial weighted noise sums from its noise tile right after
+                                          the rollouts, so that HBM read overlaps the other CTAs'
+                                          rollouts; a small kernel rescales the partials by
+                                          exp(-(m_c - S_min)/lambda) in CTA order.  Costs, noise and
+                                          k* identical; U equal up to rounding (default 1) */
 } mppi_option_t;
 
 /* mppi_set_option — execution options that never change results. */

@@ -21,6 +21,7 @@ MPPI_OPTION_CUDA_GRAPH, MPPI_OPTION_PACKED_SAMPLES, MPPI_OPTION_FUSED_NOISE, MPP
 MPPI_OPTION_BULK_REDUCTION = 5
 MPPI_OPTION_PDL = 6
 MPPI_OPTION_SPARSE_REDUCTION = 7
+MPPI_OPTION_FUSED_REDUCTION = 8
 MPPI_WEIGHTS_TRAJECTORY, MPPI_WEIGHTS_COST_TO_GO = 0, 1
 
 

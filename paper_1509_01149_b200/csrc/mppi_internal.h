@@ -93,6 +93,10 @@ struct Ctx {
     bool tma_wsum = true;           // K3 streams eps with bulk copies (MPPI_OPTION_BULK_REDUCTION)
     bool use_pdl = false;           // programmatic kernel->kernel edges in the step graph (MPPI_OPTION_PDL)
     bool sparse_wsum = false;       // K3 skips all-zero-weight column blocks (MPPI_OPTION_SPARSE_REDUCTION)
+    bool epi = true;                // packed rollout forms the weighted sums itself (MPPI_OPTION_FUSED_REDUCTION)
+    bool epi_active = false;        // set around one optimize step that uses it
+    float* d_epi = nullptr;         // [epi_nblk][T m + 4] per-CTA partials
+    int epi_nblk = 0;
     uint8_t* d_flags = nullptr;     // [ceil(K_loc m / 4 / 256)] nonzero-weight block flags
     // set around a fused launch: the rollout writes the noise it draws here (else nullptr)
     float* gen_eps = nullptr;
@@ -176,6 +180,8 @@ bool fused_noise_applies(const Ctx& c);  // the rollout kernel for c can draw it
 size_t rollout_smem_bytes(const Ctx& c, bool cells);   // dynamic smem of the rollout kernels
 size_t smem_optin_bytes();                             // the device's per-block opt-in limit
 bool grid_on(const Ctx& c);              // the obstacle candidate grid is in use
+bool epi_applies(const Ctx& c);          // the packed rollout can run the fused reduction
+cudaError_t launch_epi_combine(Ctx& c, const long long* key);
 // NCCL (mppi_nccl.cu): runtime-resolved, 0 on success, >0 ncclResult_t, -1 unavailable
 bool nccl_available();
 int nccl_unique_id(unsigned char* out);

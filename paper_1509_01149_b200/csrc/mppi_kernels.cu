@@ -172,6 +172,9 @@ struct RolloutArgs {
     const float2* cent;
     int cell_nx, cell_ny, n_cent;
     float cell_ox, cell_oy, cell_inv_h, cell_band;
+    // fused reduction (EPI): per-CTA [A_c[T][M], m_c, eta_c, pad, pad] against the CTA's minimum
+    float* epi_part;
+    float lambda;
     // fused noise (GEN kernels): eps[t][k] drawn in-kernel with the K1 counters and written here
     float* eps_out;
     unsigned step_lo, step_hi;
@@ -451,7 +454,13 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
 //
 // DIAG = false (correlated Sigma, per-step A_t of NEXT-3): du = F_t eps and the full quadratic
 // IS_t with the per-t matrices staged in shared memory, lane-wise the one-sample kernel's order.
-template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true>
+//
+// EPI: the weighted-noise sums start inside this kernel.  After its samples are rolled out, a
+// CTA weights them against ITS minimum, w = exp(-(S - m_c)/lambda), and re-reads its own noise
+// tile (written moments ago) to form eta_c and A_c[t][j]; the HBM stream of that read overlaps
+// the other CTAs' ALU-bound rollouts instead of running as a separate pass.  epi_combine_kernel
+// rescales by exp(-(m_c - S_min)/lambda) (the online-softmax identity) in a fixed order.
+template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true, bool EPI = false>
 __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
     rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
     constexpr int M = 4;
@@ -501,6 +510,7 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
 
     const int k = 2 * (blockIdx.x * blockDim.x + tid);                 // samples k, k+1
     long long key = LLONG_MAX;
+    float cost_a = 0.0f, cost_b = 0.0f;                                // (EPI)
     if (k < a.K_loc) {
         QuadrotorX2 st;
         st.load(a.x0_dev ? a.x0_dev : a.x0);
@@ -640,16 +650,105 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
         const long long ka = cost_key(sa, a.k_offset + (unsigned)k);
         const long long kb = cost_key(sb, a.k_offset + (unsigned)k + 1u);
         key = ka < kb ? ka : kb;
+        cost_a = sa;
+        cost_b = sb;
     }
     key = warp_min_ll(key);
     __shared__ long long wmin[kRolloutThreads / 32];
+    __shared__ long long sBlockKey;
     if ((tid & 31) == 0) wmin[tid >> 5] = key;
     __syncthreads();
     if (tid < 32) {
         long long v = tid < (int)(blockDim.x >> 5) ? wmin[tid] : LLONG_MAX;
         v = warp_min_ll(v);
         if (tid == 0 && v != LLONG_MAX) atomicMin(a.min_key, v);
+        if (tid == 0) sBlockKey = v;
     }
+    if constexpr (EPI) {
+        constexpr int NW = kRolloutThreads / 32;
+        __shared__ float sW[2 * kRolloutThreads];
+        __shared__ float sEta[NW];
+        const int lane = tid & 31, warp = tid >> 5;
+        __syncthreads();                                              // sBlockKey; own eps rows
+        const long long bk = sBlockKey;
+        if (bk == LLONG_MAX) return;                                  // no sample in this CTA
+        const float mc = key_cost(bk);
+        const bool va = k < a.K_loc;
+        const float wa = va ? expf(-__fdiv_rn(cost_a - mc, a.lambda)) : 0.0f;
+        const float wb = va ? expf(-__fdiv_rn(cost_b - mc, a.lambda)) : 0.0f;
+        sW[2 * tid] = wa;
+        sW[2 * tid + 1] = wb;
+        const float ew = warp_sum(wa + wb);
+        if (lane == 0) sEta[warp] = ew;
+        __syncthreads();
+        const int k0 = 2 * blockIdx.x * blockDim.x;
+        const int nk = min(2 * (int)blockDim.x, a.K_loc - k0);
+        float* part = a.epi_part + (size_t)blockIdx.x * (a.T * M + 4);   // [A (T M)][m_c, eta_c, -, -]
+        const float* eps_src = GEN ? a.eps_out : a.eps;
+        for (int t = warp; t < a.T; t += NW) {
+            const float4* row4 = reinterpret_cast<const float4*>(eps_src + ((size_t)t * a.K_loc + k0) * M);
+            float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll 4
+            for (int s2 = lane; s2 < nk; s2 += 32) {
+                const float4 e = row4[s2];
+                const float w = sW[s2];
+                acc.x = fmaf(w, e.x, acc.x);
+                acc.y = fmaf(w, e.y, acc.y);
+                acc.z = fmaf(w, e.z, acc.z);
+                acc.w = fmaf(w, e.w, acc.w);
+            }
+            // four sums across the warp in 6 shuffles (transpose-reduce, fixed order): after the
+            // offset-16 and offset-8 exchanges lane l holds component 2*(l>>4 & 1) + (l>>3 & 1)
+            const bool up = lane & 16, up2 = lane & 8;
+            float k0 = up ? acc.z : acc.x, k1 = up ? acc.w : acc.y;
+            k0 += __shfl_xor_sync(0xffffffffu, up ? acc.x : acc.z, 16);
+            k1 += __shfl_xor_sync(0xffffffffu, up ? acc.y : acc.w, 16);
+            float kk = up2 ? k1 : k0;
+            kk += __shfl_xor_sync(0xffffffffu, up2 ? k0 : k1, 8);
+            kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+            kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+            kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+            if ((lane & 7) == 0) part[t * M + (lane >> 3)] = kk;   // lanes 0, 8, 16, 24: j = 0..3
+        }
+        if (tid == 0) {
+            float eta = 0.0f;
+#pragma unroll
+            for (int w2 = 0; w2 < NW; ++w2) eta += sEta[w2];
+            part[a.T * M] = mc;
+            part[a.T * M + 1] = eta;
+        }
+    }
+}
+
+// EPI combine: the per-CTA partials of rollout_kernel_x2<..., EPI> rescaled to the global minimum
+// S_min (the min key), exp(-(S - S_min)/l) = exp(-(S - m_c)/l) exp(-(m_c - S_min)/l), summed in
+// CTA order within chunks of cpc CTAs into K4's partial layout [chunk][T][M] + [chunk] eta.
+struct EpiCombineArgs {
+    const float* epi_part;   // [nblk][T M + 4]
+    const long long* key;
+    float* part;             // [n_chunks][T M]
+    float* eta_part;         // [n_chunks]
+    int nblk, cpc, TM;
+    float lambda;
+};
+
+__global__ void __launch_bounds__(256) epi_combine_kernel(const EpiCombineArgs a) {
+    pdl_wait();
+    __shared__ float sc[256];
+    const int chunk = blockIdx.x;
+    const int c0 = chunk * a.cpc, c1 = min(a.nblk, c0 + a.cpc);
+    const size_t stride = (size_t)a.TM + 4;
+    const float smin = key_cost(*a.key);
+    for (int i = threadIdx.x; i < c1 - c0; i += blockDim.x)
+        sc[i] = expf(-__fdiv_rn(__ldg(a.epi_part + (size_t)(c0 + i) * stride + a.TM) - smin, a.lambda));
+    __syncthreads();
+    const int o = blockIdx.y * blockDim.x + threadIdx.x;   // o < TM: A[o]; o == TM: eta
+    if (o > a.TM) return;
+    const int idx = o < a.TM ? o : a.TM + 1;
+    float acc = 0.0f;
+    for (int c = c0; c < c1; ++c) acc = fmaf(sc[c - c0], __ldg(a.epi_part + (size_t)c * stride + idx), acc);
+    if (o < a.TM) a.part[(size_t)chunk * a.TM + o] = acc;
+    else a.eta_part[chunk] = acc;
 }
 
 // ------------------------------------------------------------------------------ K3 weights + GEMV
@@ -1684,7 +1783,17 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
                 kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true, true> : (const void*)rollout_kernel_x2<NP, false, true>;
             }
         } else {
-            kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
+            if constexpr (NP == kCellGrid) {
+                if (c.epi_active && c.gen_eps) {    // fused reduction (EPI)
+                    a.epi_part = c.d_epi;
+                    a.lambda = c.lambda;
+                    kern = (const void*)rollout_kernel_x2<NP, true, false, true, true>;
+                } else {
+                    kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
+                }
+            } else {
+                kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
+            }
         }
     } else {
         // cost-to-go weighting: the QSTEP variants exist for the runtime-count and grid obstacle
@@ -1783,6 +1892,28 @@ size_t smem_optin_bytes() {
 // beside the horizon's per-t records (very long horizons fall back to the full search)
 bool grid_on(const Ctx& c) {
     return c.use_cells && c.cell_nx > 0 && rollout_smem_bytes(c, true) <= smem_optin_bytes();
+}
+
+// the packed rollout's fused reduction (EPI): the C5-type path (packed quadrotor, diagonal,
+// candidate grid, in-kernel noise, trajectory weights)
+bool epi_applies(const Ctx& c) {
+    return c.epi && c.d_epi && c.plant == MPPI_PLANT_QUADROTOR && c.diag && !c.per_t && c.pack2 &&
+           !c.ctg && c.K_loc >= kPackedMinK && grid_on(c) && fused_noise_applies(c);
+}
+
+cudaError_t launch_epi_combine(Ctx& c, const long long* key) {
+    EpiCombineArgs a{};
+    a.epi_part = c.d_epi;
+    a.key = key;
+    a.part = c.d_part;
+    a.eta_part = c.d_eta_part;
+    a.nblk = c.epi_nblk;
+    a.cpc = (c.epi_nblk + c.n_chunks - 1) / c.n_chunks;
+    a.TM = c.T * c.m;
+    a.lambda = c.lambda;
+    if (a.cpc > 256) return cudaErrorInvalidValue;   // sized at create so that it is not
+    const dim3 grid((unsigned)c.n_chunks, (unsigned)((a.TM + 1 + 255) / 256));
+    return emit(c, (const void*)epi_combine_kernel, grid, dim3(256), 0, &a, sizeof(a), MPPI_KERNEL_WSUM);
 }
 
 bool fused_noise_applies(const Ctx& c) {

@@ -302,6 +302,7 @@ void free_ctx(Ctx& c) {
     cudaFree(c.d_cells);
     cudaFree(c.d_cent);
     cudaFree(c.d_flags);
+    cudaFree(c.d_epi);
     cudaFree(c.d_eps);
     cudaFree(c.d_costs);
     cudaFree(c.d_key_init);
@@ -493,6 +494,11 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
     c.cols_per_chunk = (c.cols_per_chunk + kWsumThreads - 1) / kWsumThreads * kWsumThreads;
     c.n_chunks = (int)((ncols + c.cols_per_chunk - 1) / c.cols_per_chunk);
 
+    // fused reduction (packed quadrotor): per-CTA partials, combined in chunks of <= 256 CTAs
+    if (plant == MPPI_PLANT_QUADROTOR && m == 4 && K_loc >= kPackedMinK) {
+        const int64_t nblk = (K_loc / 2 + kRolloutThreads - 1) / kRolloutThreads;
+        if ((nblk + c.n_chunks - 1) / c.n_chunks <= 256) c.epi_nblk = (int)nblk;
+    }
     mppi_status_t a;
     if ((a = dalloc(c, &c.d_eps, (size_t)T * K_loc * m, "noise")) ||
         (a = dalloc(c, &c.d_costs, (size_t)K_loc, "costs")) ||
@@ -503,6 +509,7 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
         (a = dalloc(c, &c.d_U, (size_t)T * m, "U staging")) ||
         (a = dalloc(c, &c.d_obs, (size_t)(c.n_obs_pairs > 0 ? c.n_obs_pairs : 1), "obstacles")) ||
         (a = dalloc(c, &c.d_flags, (size_t)((ncols + kWsumThreads - 1) / kWsumThreads), "weight block flags")) ||
+        (c.epi_nblk > 0 && (a = dalloc(c, &c.d_epi, (size_t)c.epi_nblk * ((size_t)T * m + 4), "fused-reduction partials"))) ||
         (!c.cells_host.empty() &&
          ((a = dalloc(c, &c.d_cells, c.cells_host.size(), "obstacle grid")) ||
           (a = dalloc(c, &c.d_cent, c.cent_host.size(), "obstacle centres"))))) {
@@ -572,6 +579,10 @@ static cudaError_t launch_reduce_update(Ctx& c, const float* eps, float* U) {
         if ((e = launch_wsum_ctg(c, eps)) != cudaSuccess) return e;
         return launch_finalize_ctg(c, U);
     }
+    if (c.epi_active) {   // the rollout formed per-CTA sums: rescale, then K4
+        if ((e = launch_epi_combine(c, &c.d_stats->min_key)) != cudaSuccess) return e;
+        return launch_finalize(c, nullptr, nullptr, U);
+    }
     if ((e = launch_wsum(c, eps, &c.d_stats->min_key)) != cudaSuccess) return e;
     return launch_finalize(c, nullptr, nullptr, U);
 }
@@ -601,6 +612,7 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
     c.collect = true;
     const float* eps = noise ? noise : c.d_eps;
     const bool fused = !noise && fused_noise_applies(c);
+    c.epi_active = !noise && epi_applies(c);
     cudaError_t e = cudaSuccess;
     if (!noise && !fused) e = launch_noise(c, seed, step, c.d_eps, true);
     if (fused) {
@@ -611,6 +623,7 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
     if (e == cudaSuccess) e = launch_rollout(c, x0, U, eps, nullptr);
     c.gen_eps = nullptr;
     if (e == cudaSuccess) e = launch_reduce_update(c, eps, U);
+    c.epi_active = false;
     c.collect = false;
     if (e != cudaSuccess) return cuda_fail(e, "collecting the step's launches");
     GraphState& G = c.graphs[noise ? 1 : 0];
@@ -682,6 +695,7 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
         case MPPI_OPTION_OBSTACLE_GRID: ctx->c.use_cells = value != 0; return MPPI_OK;
         case MPPI_OPTION_BULK_REDUCTION: ctx->c.tma_wsum = value != 0; return MPPI_OK;
         case MPPI_OPTION_SPARSE_REDUCTION: ctx->c.sparse_wsum = value != 0; return MPPI_OK;
+        case MPPI_OPTION_FUSED_REDUCTION: ctx->c.epi = value != 0; return MPPI_OK;
         case MPPI_OPTION_PDL:
             MPPI_CUDA(cudaStreamSynchronize(ctx->c.stream), "stream sync");
             ctx->c.use_pdl = value != 0;
@@ -698,7 +712,11 @@ static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t s
                                    const float* noise) {
     c.last_launches = 0;
     const float* eps = nullptr;
-    if (mppi_status_t s = do_rollout(c, x0, U, seed, step, noise, nullptr, &eps)) return s;
+    const bool epi = !noise && epi_applies(c);
+    c.epi_active = epi;
+    mppi_status_t rs = do_rollout(c, x0, U, seed, step, noise, nullptr, &eps);
+    c.epi_active = false;
+    if (rs) return rs;
     int r = nccl_min_key(c, &c.d_stats->min_key);
     if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(MIN key): %s", nccl_error(r));
     if (c.ctg) {
@@ -715,7 +733,11 @@ static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t s
         c.last_eps = eps;
         return MPPI_OK;
     }
-    MPPI_CUDA(launch_wsum(c, eps, &c.d_stats->min_key), "wsum_kernel launch");
+    if (epi) {
+        MPPI_CUDA(launch_epi_combine(c, &c.d_stats->min_key), "fused-reduction combine launch");
+    } else {
+        MPPI_CUDA(launch_wsum(c, eps, &c.d_stats->min_key), "wsum_kernel launch");
+    }
     MPPI_CUDA(launch_finalize(c, nullptr, c.d_commbuf, nullptr), "finalize (partials) launch");
     r = nccl_sum_buf(c, c.d_commbuf, (size_t)1 + (size_t)c.T * c.m);
     if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(SUM [eta, A]): %s", nccl_error(r));
@@ -754,8 +776,12 @@ mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t s
     if (c.use_graph && !c.prof) return optimize_graph(c, x0, U, seed, step, noise);
     c.last_launches = 0;
     const float* eps = nullptr;
-    if (mppi_status_t s = do_rollout(c, x0, U, seed, step, noise, nullptr, &eps)) return s;
-    MPPI_CUDA(launch_reduce_update(c, eps, U), "reduction/update launch");
+    c.epi_active = !noise && epi_applies(c);
+    mppi_status_t s = do_rollout(c, x0, U, seed, step, noise, nullptr, &eps);
+    const cudaError_t e = s ? cudaSuccess : launch_reduce_update(c, eps, U);
+    c.epi_active = false;
+    if (s) return s;
+    MPPI_CUDA(e, "reduction/update launch");
     return MPPI_OK;
 }
 

@@ -125,10 +125,17 @@ def _u_parity(oracle, w, K, lam=None, seed=1, coupled=True):
     buf = m.accumulate()
     m.apply(U, buf)
     U_gpu = U.cpu().numpy().astype(np.float64)
-    # one-shot path gives the same bits as the split phase
+    # one-shot path gives the same bits as the split phase (without the fused reduction, which
+    # associates the sums per rollout CTA: equal to rounding)
+    from paper_1509_01149_b200 import _capi as A
+    m.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
     U2 = cuda_u(w)
     m.optimize(w.x0, U2, seed, 0)
     assert torch.equal(U2, U)
+    m.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 1)
+    U3 = cuda_u(w)
+    m.optimize(w.x0, U3, seed, 0)
+    torch.testing.assert_close(U3, U, rtol=1e-6, atol=1e-6)
     pb = oracle_problem(oracle, w, lam=lam)
     # (i) decoupled: oracle reduction on the GPU's costs and noise
     Ud, kstar, smin, eta, wts = oracle.update(pb, costs.cpu().numpy().astype(np.float64), eps_gpu, w.U0)
@@ -398,6 +405,8 @@ def test_packed_two_sample_rollout_is_bitwise_scalar():
         a = from_workload(w, K=K)
         b = from_workload(w, K=K)
         b.set_option(A.MPPI_OPTION_PACKED_SAMPLES, 0)
+        b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)   # bitwise comparison: no fused reduction
+        a.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
         U = cuda_u(w)
         ca, ka = a.rollout_costs(w.x0, U, 5, 3)
         cb, kb = b.rollout_costs(w.x0, U, 5, 3)
@@ -434,6 +443,8 @@ def test_packed_out_of_fast_range_replay_is_bitwise_scalar(yaw, rate):
     a = from_workload(w, K=1 << 16)
     b = from_workload(w, K=1 << 16)
     b.set_option(A.MPPI_OPTION_PACKED_SAMPLES, 0)
+    b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)   # bitwise comparison: no fused reduction
+    a.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
     U = cuda_u(w)
     ca, ka = a.rollout_costs(x0, U, 7, 1)
     cb, kb = b.rollout_costs(x0, U, 7, 1)
@@ -454,6 +465,8 @@ def test_fused_noise_rollout_is_bitwise_separate_pass(cfg, T, Ks):
         a = from_workload(w, K=K)
         b = from_workload(w, K=K)
         b.set_option(A.MPPI_OPTION_FUSED_NOISE, 0)
+        b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)   # bitwise comparison: no fused reduction
+        a.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
         U = cuda_u(w)
         ca, ka = a.rollout_costs(w.x0, U, 11, 4)
         cb, kb = b.rollout_costs(w.x0, U, 11, 4)
@@ -500,6 +513,8 @@ def test_bulk_copy_reduction_is_bitwise_plain_loads(cfg, K):
         a = from_workload(w, K=K)
         b = from_workload(w, K=K)
         b.set_option(A.MPPI_OPTION_BULK_REDUCTION, 0)
+        b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)   # bitwise comparison: no fused reduction
+        a.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
         if ctg:
             a.set_weighting(True)
             b.set_weighting(True)
@@ -526,6 +541,8 @@ def test_sparse_reduction_is_bitwise_dense(cfg, K, lam):
     a = from_workload(w, K=K)
     b = from_workload(w, K=K)
     a.set_option(A.MPPI_OPTION_SPARSE_REDUCTION, 1)
+    a.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)   # bitwise comparison: no fused reduction
+    b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
     for graph in (True, False):
         a.use_graph(graph)
         Ua, Ub = cuda_u(w), cuda_u(w)
@@ -554,12 +571,17 @@ def test_general_sigma_fast_paths_are_bitwise(cfg):
                       obstacles=w.obstacles if w.plant == "quadrotor" else None)
     a, b = mk(), mk()
     b.set_option(A.MPPI_OPTION_FUSED_NOISE, 0)
+    b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)   # bitwise comparison: no fused reduction
+    a.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
     if w.plant == "quadrotor":
         b.set_option(A.MPPI_OPTION_OBSTACLE_GRID, 0)
+        b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)   # bitwise comparison: no fused reduction
+        a.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
     variants = [b]
     if w.plant == "quadrotor":                      # packed general-Sigma kernel vs one-sample
         c = mk()
         c.set_option(A.MPPI_OPTION_PACKED_SAMPLES, 0)
+        c.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)   # bitwise comparison: no fused reduction
         variants.append(c)
     U = cuda_u(w)
     ca, ka = a.rollout_costs(w.x0, U, 6, 2)
@@ -586,6 +608,8 @@ def test_longest_horizon():
     a = from_workload(w, K=1 << 16)
     b = from_workload(w, K=1 << 16)
     b.set_option(A.MPPI_OPTION_PACKED_SAMPLES, 0)
+    b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)   # bitwise comparison: no fused reduction
+    a.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
     U = cuda_u(w)
     ca, ka = a.rollout_costs(w.x0, U, 1, 0)
     cb, kb = b.rollout_costs(w.x0, U, 1, 0)
@@ -597,6 +621,34 @@ def test_longest_horizon():
     Sig = np.array(w.Sigma, np.float64) + 1e-4
     with pytest.raises(MppiError):
         MPPI(w.plant, 1 << 16, 4096, w.dt, w.lam, w.nu, Sig, w.R, obstacles=w.obstacles)
+
+
+@pytest.mark.parametrize("K,lam", [(65536 + 4, None), (65536 + 4, 1e6), (1 << 18, 1e7), (1 << 18, 30.0)])
+def test_fused_reduction_matches_separate_reduction(K, lam):
+    """MPPI_OPTION_FUSED_REDUCTION: per-CTA weights against the CTA minimum, rescaled by
+    exp(-(m_c - S_min)/lambda) in CTA order, give the separate reduction's update to rounding
+    (one-hot weights at the config's lambda, nearly uniform ones at lambda = 1e6..1e7), with the
+    same costs and k*, step after step, graph and direct launches."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get("C4")
+    if lam is not None:
+        w.lam = lam
+    a = from_workload(w, K=K)
+    b = from_workload(w, K=K)
+    b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
+    for graph in (True, False):
+        a.use_graph(graph)
+        Ua, Ub = cuda_u(w), cuda_u(w)
+        for i in range(3):
+            a.optimize(w.x0, Ua, 5, i)
+            b.optimize(w.x0, Ub, 5, i)
+            sa, sb = a.stats(), b.stats()
+            assert sa["k_star"] == sb["k_star"] and sa["s_min"] == sb["s_min"]
+            assert sa["eta"] == pytest.approx(sb["eta"], rel=1e-5)
+            torch.testing.assert_close(Ua, Ub, rtol=1e-5, atol=1e-6)
+            Ub.copy_(Ua)
+    a.close()
+    b.close()
 
 
 @pytest.mark.parametrize("xy", [(0.0, 0.0), (25.0, 1.5), (44.0, -9.0), (300.0, 0.0), (-60.0, 80.0), (5000.0, 5.0)])
@@ -612,6 +664,8 @@ def test_obstacle_grid_is_bitwise_full_search(xy):
     a = from_workload(w, K=1 << 16)
     b = from_workload(w, K=1 << 16)
     b.set_option(A.MPPI_OPTION_OBSTACLE_GRID, 0)
+    b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)   # bitwise comparison: no fused reduction
+    a.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
     U = cuda_u(w)
     for seed in (1, 2):
         ca, ka = a.rollout_costs(x0, U, seed, 0)
