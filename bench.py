@@ -642,6 +642,12 @@ def main():
                  "device_closed_loop": device_closed_loop("C2"),
                  "fig1_trend": fig1_trend()}
 
+    if extra and args.config == "C5" and not args.K:
+        sep = (extra.get("C5_separate_reduction") or {}).get("kernel_avg_ms") or {}
+        if "wsum_hbm_GBps" in sep:   # the dense K x (T m) GEMV as its own kernel (same workload)
+            roof["secondary"]["separate_wsum_ms"] = sep["wsum"]
+            roof["secondary"]["separate_wsum_hbm_GBps"] = sep["wsum_hbm_GBps"]
+            roof["secondary"]["separate_wsum_hbm_frac"] = sep["wsum_hbm_frac"]
     eps_bytes = 4 * w.T * K_loc * w.m
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

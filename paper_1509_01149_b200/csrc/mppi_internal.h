@@ -19,6 +19,9 @@ constexpr int kWsumThreads = 256;
 #ifndef MPPI_X2_MINB
 #define MPPI_X2_MINB 4
 #endif
+#ifndef MPPI_EPI_ROWS
+#define MPPI_EPI_ROWS 2      // fused-reduction epilogue: noise rows per warp pass (8 float4 loads each)
+#endif
 constexpr int kWsumTT = 8;                      // timestep rows per reduction CTA
 #ifndef MPPI_WSUM_STAGES
 #define MPPI_WSUM_STAGES 2

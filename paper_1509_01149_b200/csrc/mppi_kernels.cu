@@ -685,20 +685,9 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
         const int nk = min(2 * (int)blockDim.x, a.K_loc - k0);
         float* part = a.epi_part + (size_t)blockIdx.x * (a.T * M + 4);   // [A (T M)][m_c, eta_c, -, -]
         const float* eps_src = GEN ? a.eps_out : a.eps;
-        for (int t = warp; t < a.T; t += NW) {
-            const float4* row4 = reinterpret_cast<const float4*>(eps_src + ((size_t)t * a.K_loc + k0) * M);
-            float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-#pragma unroll 4
-            for (int s2 = lane; s2 < nk; s2 += 32) {
-                const float4 e = row4[s2];
-                const float w = sW[s2];
-                acc.x = fmaf(w, e.x, acc.x);
-                acc.y = fmaf(w, e.y, acc.y);
-                acc.z = fmaf(w, e.z, acc.z);
-                acc.w = fmaf(w, e.w, acc.w);
-            }
-            // four sums across the warp in 6 shuffles (transpose-reduce, fixed order): after the
-            // offset-16 and offset-8 exchanges lane l holds component 2*(l>>4 & 1) + (l>>3 & 1)
+        // four sums across the warp in 6 shuffles (transpose-reduce, fixed order): after the
+        // offset-16 and offset-8 exchanges lane l holds component 2*(l>>4 & 1) + (l>>3 & 1)
+        auto reduce_store = [&](const float4 acc, int t) {
             const bool up = lane & 16, up2 = lane & 8;
             float k0 = up ? acc.z : acc.x, k1 = up ? acc.w : acc.y;
             k0 += __shfl_xor_sync(0xffffffffu, up ? acc.x : acc.z, 16);
@@ -709,6 +698,50 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
             kk += __shfl_xor_sync(0xffffffffu, kk, 2);
             kk += __shfl_xor_sync(0xffffffffu, kk, 1);
             if ((lane & 7) == 0) part[t * M + (lane >> 3)] = kk;   // lanes 0, 8, 16, 24: j = 0..3
+        };
+        auto fma4 = [](float4& acc, float w, const float4 e) {   // two FFMA2 (same per-lane fma)
+            const float2 ww = make_float2(w, w);
+            const float2 lo = __ffma2_rn(ww, make_float2(e.x, e.y), make_float2(acc.x, acc.y));
+            const float2 hi = __ffma2_rn(ww, make_float2(e.z, e.w), make_float2(acc.z, acc.w));
+            acc = make_float4(lo.x, lo.y, hi.x, hi.y);
+        };
+        if (nk == 2 * kRolloutThreads) {
+            // full CTA: the lane's 8 weights in registers, MPPI_EPI_ROWS rows (8 independent 16-byte
+            // loads each) in flight per lane -- the re-read comes from HBM, so the epilogue is
+            // latency-bound on how many loads a warp has outstanding.  Same summation order as
+            // the loop below.
+            constexpr int J = 2 * kRolloutThreads / 32;
+            float wr[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) wr[j] = sW[lane + 32 * j];
+            auto rows = [&](auto RN, int t) {
+                constexpr int R = decltype(RN)::value;
+                const float4* r0 = reinterpret_cast<const float4*>(eps_src + ((size_t)t * a.K_loc + k0) * M);
+                float4 e[R][J];
+#pragma unroll
+                for (int j = 0; j < J; ++j)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) e[r][j] = __ldcs(r0 + (size_t)r * NW * a.K_loc + lane + 32 * j);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+                    for (int j = 0; j < J; ++j) fma4(acc, wr[j], e[r][j]);
+                    reduce_store(acc, t + r * NW);
+                }
+            };
+            int t = warp;
+            for (; t + (MPPI_EPI_ROWS - 1) * NW < a.T; t += MPPI_EPI_ROWS * NW)
+                rows(std::integral_constant<int, MPPI_EPI_ROWS>(), t);
+            for (; t < a.T; t += NW) rows(std::integral_constant<int, 1>(), t);
+        } else {
+            for (int t = warp; t < a.T; t += NW) {
+                const float4* row4 = reinterpret_cast<const float4*>(eps_src + ((size_t)t * a.K_loc + k0) * M);
+                float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll 4
+                for (int s2 = lane; s2 < nk; s2 += 32) fma4(acc, sW[s2], row4[s2]);
+                reduce_store(acc, t);
+            }
         }
         if (tid == 0) {
             float eta = 0.0f;
