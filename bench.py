@@ -40,9 +40,9 @@ ROLLOUT_FLOP_PER_SS = {"cartpole": 59.43, "racecar": 249.6,   # profiles/r1_roll
 FUSED_QUAD = {"flop": 358.10, "inst": 311.85, "dram_bytes": 15.953}
 # The same kernel with the fused reduction epilogue (MPPI_OPTION_FUSED_REDUCTION, the default):
 # each CTA also forms its samples' weights and weighted noise sums, re-reading the noise it wrote
-# (profiles/r1_ncu_full_c5_v14.txt).  Algorithmic bytes: the noise written and read back once,
-# 2 * 4 m per sample-step.
-FUSED_QUAD_EPI = {"flop": 366.99, "inst": 328.17, "dram_bytes": 32.07}
+# (profiles/r1_ncu_full_c5_v15.txt).  Algorithmic bytes: the noise written and read back once,
+# 2 * 4 m per sample-step (ncu DRAM bytes are below that: part of the re-read hits L2).
+FUSED_QUAD_EPI = {"flop": 366.99, "inst": 320.43, "dram_bytes": 27.84}
 
 
 def rollout_variant(w, K_loc, fused_reduction=True):
