@@ -45,9 +45,40 @@ FUSED_QUAD = {"flop": 358.10, "inst": 311.85, "dram_bytes": 15.953}
 FUSED_QUAD_EPI = {"flop": 366.99, "inst": 320.43, "dram_bytes": 27.84}
 
 
-def rollout_variant(w, K_loc, fused_reduction=True):
-    """Which rollout kernel bench.py's configuration runs (mirrors dispatch_np/fused_noise_applies/
-    epi_applies)."""
+def variant_of(kernels):
+    """The rollout variant the library's dispatch chose, from the mangled device-function names
+    of the last step's launches (mppi_last_kernels): rollout_kernel_x2<NP, GEN, QSTEP, DIAG, EPI>
+    -> "x2[-grid][-fused][-general][-ctg][-epi]", the one-sample kernels -> "scalar"."""
+    import re
+    for k in kernels:
+        mt = re.search(r"rollout_kernel_x2IL(in?)(\d+)ELb([01])ELb([01])ELb([01])ELb([01])E", k)
+        if mt:
+            np_ = -int(mt.group(2)) if mt.group(1) == "in" else int(mt.group(2))
+            gen, qstep, diag, epi = (mt.group(i) == "1" for i in range(3, 7))
+            return ("x2" + ("-grid" if np_ == -2 else "") + ("-fused" if gen else "") +
+                    ("" if diag else "-general") + ("-ctg" if qstep else "") + ("-epi" if epi else ""))
+        if "rollout_kernel" in k:
+            return "scalar"
+    return None
+
+
+def short_names(kernels):
+    """_ZN4mppi17rollout_kernel_x2ILin2E... -> rollout_kernel_x2 (the identifier only)."""
+    import re
+    out = []
+    for k in kernels:
+        mt = re.match(r"_ZN4mppi(\d+)", k)
+        out.append(k[mt.end():mt.end() + int(mt.group(1))] if mt else k)
+    return out
+
+
+def rollout_variant(w, K_loc, fused_reduction=True, m=None):
+    """Which rollout kernel bench.py's configuration runs: asked from the library when a context
+    that has stepped is given, else predicted (mirrors dispatch_np/fused_noise_applies/epi_applies)."""
+    if m is not None:
+        v = variant_of(m.last_kernels())
+        if v is not None:
+            return v
     if w.plant == "quadrotor" and K_loc >= 65536 and w.obstacles is not None and len(w.obstacles) >= 2:
         return "x2-grid-fused-epi" if fused_reduction else "x2-grid-fused"
     return "scalar"
@@ -317,6 +348,7 @@ def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=Fals
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
+    launched = m.last_kernels()
     kern = None
     if profile:     # a separate profiled pass (per-kernel CUDA events), after the timed one
         m.profile_enable(True)
@@ -334,10 +366,10 @@ def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=Fals
     return {"plant": w.plant, "K": K or w.K, "T": w.T, "ms_per_step": ms, "kernel_avg_ms": kern,
             "KT_per_s": (K or w.K) * w.T / (ms * 1e-3),
             "weighting": "cost-to-go (PAPER.md:320-322)" if cost_to_go else "trajectory",
-            "rollout": rollout_variant(w, K or w.K, fused_reduction and not sparse),
+            "rollout": variant_of(launched), "kernels": short_names(launched),
             "reduction": ("sparse (all-zero weight blocks skipped, bit-identical)" if sparse else
-                          "fused into the rollout" if rollout_variant(w, K or w.K, fused_reduction)
-                          .endswith("-epi") else "dense GEMV")}
+                          "fused into the rollout" if any("epi_combine" in k for k in launched)
+                          else "dense GEMV")}
 
 
 def c_abi_closed_loop(steps=200):
@@ -504,6 +536,7 @@ def main():
         dist.barrier()
     ms = e0.elapsed_time(e1)
     ktimes = m.profile_read()
+    launched = m.last_kernels()     # the kernel sequence of one timed step
     m.profile_enable(False)
     clk = clocks.stop()
     launches = sum(v[1] for v in ktimes.values())
@@ -573,10 +606,10 @@ def main():
     avg_s = kern[dom]["avg_ms"] * 1e-3
     K_loc = K // world
     roof = {"kernel": dom}
-    variant_of_step = rollout_variant(w, K_loc)
+    variant_of_step = variant_of(launched) or rollout_variant(w, K_loc)
     if dom == "rollout":
         fp = fp32_peak(probe, props.multi_processor_count, sm_max)
-        variant = rollout_variant(w, K_loc)
+        variant = variant_of_step
         fused = variant.startswith("x2-grid-fused")
         fq = FUSED_QUAD_EPI if variant.endswith("-epi") else FUSED_QUAD
         fl = fq["flop"] if fused else ROLLOUT_FLOP_PER_SS.get(w.plant)
@@ -662,6 +695,7 @@ def main():
                                                           "in-library NCCL MIN + SUM allreduce" if lib_nccl else
                                                           "MIN + SUM allreduce via torch.distributed")},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "kernel_sequence": short_names(launched),
         "clocks": clk, "kernels": kern, "latency": lat, "extra": extra,
         "device": torch.cuda.get_device_name(dev),
         "backend": args.backend if world > 1 else None,

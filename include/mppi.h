@@ -468,6 +468,13 @@ mppi_status_t mppi_get_stats(mppi_ctx* ctx, mppi_stats_t* out /* HOST */);
 /* Number of kernels the last mppi_optimize / split-phase call enqueued (for launch accounting). */
 int32_t mppi_last_launch_count(const mppi_ctx* ctx);
 
+/* mppi_last_kernels — the kernels the last mppi_optimize / split-phase call enqueued, in launch
+ * order, as their (mangled) device-function names separated by ',' (which kernel variant the
+ * dispatch chose: packed / fused noise / obstacle grid / fused reduction ...).
+ *   buf : HOST char [len], receives a NUL-terminated string, truncated to len - 1 characters.
+ * Returns the full length needed (excluding the NUL), or -1 for NULL ctx / buf or len < 1. */
+int64_t mppi_last_kernels(const mppi_ctx* ctx, char* buf, int64_t len);
+
 /* ---------------------------------------------------------------- per-kernel device time */
 
 typedef enum {

@@ -106,7 +106,7 @@ EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_
            "mppi_shift", "mppi_noise", "mppi_feynman_kac", "mppi_closed_loop", "mppi_set_weighting",
            "mppi_cost_to_go", "mppi_set_sampling_transform", "mppi_nccl_unique_id", "mppi_nccl_attach",
            "mppi_obstacle_grid", "mppi_plant_step", "mppi_get_stats",
-           "mppi_last_launch_count", "mppi_profile_enable", "mppi_profile_read", "mppi_last_error", "mppi_status_string", "mppi_abi_version"]
+           "mppi_last_launch_count", "mppi_last_kernels", "mppi_profile_enable", "mppi_profile_read", "mppi_last_error", "mppi_status_string", "mppi_abi_version"]
 
 _lib = None
 
@@ -174,6 +174,8 @@ def lib():
     L.mppi_get_stats.restype = st
     L.mppi_last_launch_count.argtypes = [vp]
     L.mppi_last_launch_count.restype = C.c_int32
+    L.mppi_last_kernels.argtypes = [vp, C.c_char_p, C.c_int64]
+    L.mppi_last_kernels.restype = C.c_int64
     L.mppi_profile_enable.argtypes = [vp, C.c_int32]
     L.mppi_profile_enable.restype = st
     L.mppi_profile_read.argtypes = [vp, C.POINTER(kernel_times_t)]

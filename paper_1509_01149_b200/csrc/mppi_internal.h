@@ -140,6 +140,7 @@ struct Ctx {
     int64_t cols_per_chunk = 0;     // float4 columns of a noise row per chunk
     size_t workspace_bytes = 0;
     int last_launches = 0;
+    std::vector<const void*> last_funcs;  // device functions of the last call's launches
     const float* last_eps = nullptr;  // noise read by the last rollout (ctx or caller buffer)
     // per-kernel CUDA-event timing (mppi_profile_enable)
     bool prof = false;

@@ -1688,6 +1688,7 @@ cudaError_t emit(Ctx& c, const void* func, dim3 grid, dim3 block, size_t smem, c
                  size_t size, int kind) {
     if (size > sizeof(KLaunch::args)) return cudaErrorInvalidValue;
     c.last_launches++;
+    c.last_funcs.push_back(func);
     if (c.collect) {
         c.pending.emplace_back();
         KLaunch& L = c.pending.back();
@@ -1806,8 +1807,15 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     const void* kern;
     if constexpr (X2 && !DIAG) {   // general Sigma / A_t: grid path only
         static_assert(NP == kCellGrid, "packed general-Sigma kernel: candidate-grid path only");
-        if (c.ctg) kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true, true, false> : (const void*)rollout_kernel_x2<NP, false, true, false>;
-        else kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true, false, false> : (const void*)rollout_kernel_x2<NP, false, false, false>;
+        if (c.ctg) {
+            kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true, true, false> : (const void*)rollout_kernel_x2<NP, false, true, false>;
+        } else if (c.epi_active && c.gen_eps) {   // fused reduction (EPI): the same sum of eps
+            a.epi_part = c.d_epi;
+            a.lambda = c.lambda;
+            kern = (const void*)rollout_kernel_x2<NP, true, false, false, true>;
+        } else {
+            kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true, false, false> : (const void*)rollout_kernel_x2<NP, false, false, false>;
+        }
     } else if constexpr (X2) {
         if (c.ctg) {
             if constexpr (NP >= 0) {
@@ -1930,7 +1938,8 @@ bool grid_on(const Ctx& c) {
 // the packed rollout's fused reduction (EPI): the C5-type path (packed quadrotor, diagonal,
 // candidate grid, in-kernel noise, trajectory weights)
 bool epi_applies(const Ctx& c) {
-    return c.epi && c.d_epi && c.plant == MPPI_PLANT_QUADROTOR && c.diag && !c.per_t && c.pack2 &&
+    // (diagonal or general Sigma / A_t: both packed variants sum the standard-normal eps)
+    return c.epi && c.d_epi && c.plant == MPPI_PLANT_QUADROTOR && c.pack2 &&
            !c.ctg && c.K_loc >= kPackedMinK && grid_on(c) && fused_noise_applies(c);
 }
 

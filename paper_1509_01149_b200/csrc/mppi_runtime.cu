@@ -608,6 +608,7 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
     if (!all_finite(x0, c.n)) return fail(MPPI_ERR_INVALID_ARG, "x0 must be finite");
     if (mppi_status_t s = sticky_check(c)) return s;
     c.last_launches = 0;
+    c.last_funcs.clear();
     c.pending.clear();
     c.collect = true;
     const float* eps = noise ? noise : c.d_eps;
@@ -711,6 +712,7 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
 static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t seed, uint64_t step,
                                    const float* noise) {
     c.last_launches = 0;
+    c.last_funcs.clear();
     const float* eps = nullptr;
     const bool epi = !noise && epi_applies(c);
     c.epi_active = epi;
@@ -775,6 +777,7 @@ mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t s
                                   "(or use the split-phase calls)");
     if (c.use_graph && !c.prof) return optimize_graph(c, x0, U, seed, step, noise);
     c.last_launches = 0;
+    c.last_funcs.clear();
     const float* eps = nullptr;
     c.epi_active = !noise && epi_applies(c);
     mppi_status_t s = do_rollout(c, x0, U, seed, step, noise, nullptr, &eps);
@@ -904,6 +907,7 @@ mppi_status_t mppi_rollout_costs(mppi_ctx* ctx, const float* x0, const float* U,
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
     c.last_launches = 0;
+    c.last_funcs.clear();
     const float* eps = nullptr;
     if (mppi_status_t s = do_rollout(c, x0, U, seed, step, noise, costs, &eps)) return s;
     c.last_eps = eps;  // mppi_accumulate reads the same noise again
@@ -921,6 +925,7 @@ mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, floa
                            "weighting shard through mppi_nccl_attach + mppi_optimize");
     if (mppi_status_t s = sticky_check(c)) return s;
     c.last_launches = 0;
+    c.last_funcs.clear();
     const long long* key = global_min_key ? (const long long*)global_min_key : &c.d_stats->min_key;
     MPPI_CUDA(launch_wsum(c, c.last_eps ? c.last_eps : c.d_eps, key), "wsum_kernel launch");
     MPPI_CUDA(launch_finalize(c, nullptr, buf, nullptr), "finalize_kernel launch");
@@ -936,6 +941,7 @@ mppi_status_t mppi_apply(mppi_ctx* ctx, float* U, const float* buf) {
     if (!U || !buf) return fail(MPPI_ERR_INVALID_ARG, "U and buf must be non-NULL");
     if (mppi_status_t s = sticky_check(c)) return s;
     c.last_launches = 0;
+    c.last_funcs.clear();
     MPPI_CUDA(launch_finalize(c, buf, nullptr, U), "finalize_kernel launch");
     return MPPI_OK;
 }
@@ -947,6 +953,7 @@ mppi_status_t mppi_shift(mppi_ctx* ctx, float* U, const float* u_init) {
     if (!all_finite(u_init, c.m)) return fail(MPPI_ERR_INVALID_ARG, "u_init must be finite");
     if (mppi_status_t s = sticky_check(c)) return s;
     c.last_launches = 0;
+    c.last_funcs.clear();
     MPPI_CUDA(launch_shift(c, U, u_init), "shift_kernel launch");
     return MPPI_OK;
 }
@@ -957,6 +964,7 @@ mppi_status_t mppi_noise(mppi_ctx* ctx, uint64_t seed, uint64_t step, float* out
     if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
     if (mppi_status_t s = sticky_check(c)) return s;
     c.last_launches = 0;
+    c.last_funcs.clear();
     MPPI_CUDA(launch_noise(c, seed, step, out, false), "noise_kernel launch");
     return MPPI_OK;
 }
@@ -1009,6 +1017,21 @@ mppi_status_t mppi_get_stats(mppi_ctx* ctx, mppi_stats_t* out) {
 
 int32_t mppi_last_launch_count(const mppi_ctx* ctx) { return ctx ? ctx->c.last_launches : 0; }
 
+int64_t mppi_last_kernels(const mppi_ctx* ctx, char* buf, int64_t len) {
+    if (!ctx || !buf || len < 1) return -1;
+    std::string names;
+    for (const void* f : ctx->c.last_funcs) {
+        const char* nm = nullptr;
+        if (cudaFuncGetName(&nm, f) != cudaSuccess || !nm) nm = "?";
+        if (!names.empty()) names += ',';
+        names += nm;
+    }
+    const size_t n = std::min((size_t)(len - 1), names.size());
+    memcpy(buf, names.data(), n);
+    buf[n] = '\0';
+    return (int64_t)names.size();
+}
+
 mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed, uint64_t step0,
                                int32_t n_steps, const float* u_init, int32_t reset_crash,
                                float* x_log, float* u_log, float* q_log) {
@@ -1023,6 +1046,7 @@ mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed,
         MPPI_CUDA(cudaMemsetAsync(&c.d_stats->plant_crashed, 0, sizeof(int), c.stream), "crash reset");
     // collect n_steps x [noise, rollout (x0 from device), wsum, finalize, advance] into one graph
     c.last_launches = 0;
+    c.last_funcs.clear();
     c.pending.clear();
     c.collect = true;
     c.x0_on_device = true;
@@ -1067,6 +1091,7 @@ mppi_status_t mppi_feynman_kac(mppi_ctx* ctx, const float* x0, uint64_t seed, ui
     if (c.nu != 1.0f) return fail(MPPI_ERR_UNSUPPORTED, "mppi_feynman_kac samples the uncontrolled "
                                   "dynamics P: create the context with nu == 1");
     c.last_launches = 0;
+    c.last_funcs.clear();
     // U = 0 (uncontrolled dynamics) in the context's staging buffer
     MPPI_CUDA(cudaMemsetAsync(c.d_U, 0, (size_t)c.T * c.m * sizeof(float), c.stream), "U = 0");
     const float* eps = nullptr;

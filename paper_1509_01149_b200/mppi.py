@@ -261,6 +261,17 @@ class MPPI:
     def last_launch_count(self):
         return self.lib.mppi_last_launch_count(self.ctx)
 
+    def last_kernels(self):
+        """Device-function names of the last call's kernel launches, in launch order."""
+        n = 4096
+        buf = C.create_string_buffer(n)
+        need = self.lib.mppi_last_kernels(self.ctx, buf, n)
+        if need >= n:
+            buf = C.create_string_buffer(need + 1)
+            self.lib.mppi_last_kernels(self.ctx, buf, need + 1)
+        s = buf.value.decode()
+        return s.split(",") if s else []
+
 
 def from_workload(w, K=None, world=1, rank=0, **kw):
     """MPPI context for an mppi_inputs.Workload (configs C1-C5)."""

@@ -623,18 +623,28 @@ def test_longest_horizon():
         MPPI(w.plant, 1 << 16, 4096, w.dt, w.lam, w.nu, Sig, w.R, obstacles=w.obstacles)
 
 
-@pytest.mark.parametrize("K,lam", [(65536 + 4, None), (65536 + 4, 1e6), (1 << 18, 1e7), (1 << 18, 30.0)])
-def test_fused_reduction_matches_separate_reduction(K, lam):
+@pytest.mark.parametrize("K,lam,sampling", [(65536 + 4, None, "diag"), (65536 + 4, 1e6, "diag"),
+                                             (1 << 18, 1e7, "diag"), (1 << 18, 30.0, "diag"),
+                                             (65536 + 4, 30.0, "corr"), (1 << 17, 1e6, "A_t")])
+def test_fused_reduction_matches_separate_reduction(K, lam, sampling):
     """MPPI_OPTION_FUSED_REDUCTION: per-CTA weights against the CTA minimum, rescaled by
     exp(-(m_c - S_min)/lambda) in CTA order, give the separate reduction's update to rounding
     (one-hot weights at the config's lambda, nearly uniform ones at lambda = 1e6..1e7), with the
-    same costs and k*, step after step, graph and direct launches."""
+    same costs and k*, step after step, graph and direct launches; diagonal Sigma, a correlated
+    Sigma and per-step transforms A_t (the packed kernel's general variant)."""
     from paper_1509_01149_b200 import _capi as A
     w = get("C4")
     if lam is not None:
         w.lam = lam
+    if sampling == "corr":
+        w.Sigma = np.array(w.Sigma, np.float64) + 0.001 * (np.ones((w.m, w.m)) - np.eye(w.m))
     a = from_workload(w, K=K)
     b = from_workload(w, K=K)
+    if sampling == "A_t":
+        rng = np.random.default_rng(3)
+        At = np.array([rng.normal(size=(w.m, w.m)) * 0.2 + 1.2 * np.eye(w.m) for _ in range(w.T)])
+        a.set_sampling_transform(At)
+        b.set_sampling_transform(At)
     b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
     for graph in (True, False):
         a.use_graph(graph)
@@ -642,6 +652,9 @@ def test_fused_reduction_matches_separate_reduction(K, lam):
         for i in range(3):
             a.optimize(w.x0, Ua, 5, i)
             b.optimize(w.x0, Ub, 5, i)
+            ka, kb = a.last_kernels(), b.last_kernels()
+            assert any("epi_combine" in n for n in ka) and not any("wsum" in n for n in ka), ka
+            assert any("wsum" in n for n in kb) and not any("epi_combine" in n for n in kb), kb
             sa, sb = a.stats(), b.stats()
             assert sa["k_star"] == sb["k_star"] and sa["s_min"] == sb["s_min"]
             assert sa["eta"] == pytest.approx(sb["eta"], rel=1e-5)
