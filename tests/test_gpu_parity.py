@@ -135,11 +135,14 @@ def _u_parity(oracle, w, K, lam=None, seed=1, coupled=True):
     m.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 1)
     U3 = cuda_u(w)
     m.optimize(w.x0, U3, seed, 0)
+    if w.plant == "quadrotor" and K >= 65536:
+        assert any("epi_combine" in n for n in m.last_kernels())
     torch.testing.assert_close(U3, U, rtol=1e-6, atol=1e-6)
     pb = oracle_problem(oracle, w, lam=lam)
     # (i) decoupled: oracle reduction on the GPU's costs and noise
     Ud, kstar, smin, eta, wts = oracle.update(pb, costs.cpu().numpy().astype(np.float64), eps_gpu, w.U0)
     assert np.max(np.abs(U_gpu - Ud)) <= U_ATOL
+    assert np.max(np.abs(U3.cpu().numpy().astype(np.float64) - Ud)) <= U_ATOL
     st = m.stats()
     assert st["k_star"] == kstar
     # (ii) coupled: the full fp64 oracle step, asserted when the first-order bound permits
@@ -164,6 +167,14 @@ def test_update_c3_racecar(oracle):
 
 def test_update_c4_quadrotor(oracle):
     _u_parity(oracle, get("C4"), 4096)
+
+
+@pytest.mark.parametrize("lam", [None, 30.0])
+def test_update_packed_fused_path(oracle, lam):
+    """K = 65536 + 256 (the packed kernel with in-kernel noise and the fused reduction, a ragged
+    last CTA): U against the oracle's reduction of the GPU's costs and noise, at the config's
+    lambda (one-hot weights) and at lambda = 30 (many samples weighted)."""
+    _u_parity(oracle, get("C4"), 65536 + 256, lam=lam)
 
 
 @pytest.mark.parametrize("cfg", ["C1", "C3", "C4"])
@@ -366,10 +377,27 @@ def test_full_size_c5_sampled(oracle):
     buf = m.accumulate()
     Us = cuda_u(w)
     m.apply(Us, buf)
+    from paper_1509_01149_b200 import _capi as A
+    m.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)       # the separate GEMV: the split phase's bits
     U2 = cuda_u(w)
     m.optimize(w.x0, U2, w.seed, 0)
     assert torch.equal(Us, U2) and torch.isfinite(U2).all()
     assert m.stats()["k_star"] == kk
+    m.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 1)       # the bench's path: fused reduction
+    U3 = cuda_u(w)
+    m.optimize(w.x0, U3, w.seed, 0)
+    assert any("epi_combine" in n for n in m.last_kernels())
+    assert m.stats()["k_star"] == kk
+    # decoupled oracle update at full size: every sample whose fp64 weight exceeds 1e-30 goes to
+    # the oracle's reduction (S_min is among them, so its weights are the full set's; the dropped
+    # ones change eta and A by < K * 1e-30 relative)
+    c64 = c.astype(np.float64)
+    keep = np.nonzero(np.exp(-(c64 - c64.min()) / w.lam) > 1e-30)[0]
+    eps_keep = eps[:, torch.as_tensor(keep, device=eps.device), :].cpu().numpy()
+    Ud, kstar, _, _, _ = oracle.update(pb, c64[keep], eps_keep, w.U0)
+    assert int(keep[kstar]) == kk
+    for Ux in (U2, U3):
+        assert np.max(np.abs(Ux.cpu().numpy().astype(np.float64) - Ud)) <= U_ATOL
 
 
 def test_graph_replay_matches_direct_launches():
