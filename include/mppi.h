@@ -300,8 +300,9 @@ typedef enum {
                                           the reduction then reads kilobytes instead of 4 T K m bytes.
                                           Default 0: bench.py measures the dense GEMV the north_star
                                           defines and reports this mode beside it */
-    MPPI_OPTION_FUSED_REDUCTION = 8    /* packed quadrotor path (diagonal Sigma and R, obstacle grid,
-                                          in-kernel noise, trajectory weights): every rollout CTA
+    MPPI_OPTION_FUSED_REDUCTION = 8    /* packed quadrotor path (K_loc >= 65536, diagonal or general
+                                          Sigma / A_t, obstacle grid, in-kernel noise, trajectory
+                                          weights; mppi_last_kernels shows whether it ran): every rollout CTA
                                           weights its samples against its own minimum and forms its
                                           partial weighted noise sums from its noise tile right after
                                           the rollouts, so that HBM read overlaps the other CTAs'
@@ -310,7 +311,7 @@ typedef enum {
                                           k* identical; U equal up to rounding (default 1) */
 } mppi_option_t;
 
-/* mppi_set_option — execution options that never change results. */
+/* mppi_set_option — execution options that never change results (FUSED_REDUCTION: U to rounding). */
 mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value);
 
 /* mppi_optimize_host — the same step end to end from HOST buffers: copies x0 and U in,
