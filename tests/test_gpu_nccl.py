@@ -16,9 +16,14 @@ from mppi_inputs import get  # noqa: E402
 from paper_1509_01149_b200 import MppiError, from_workload  # noqa: E402
 
 
-@pytest.mark.parametrize("cfg,K", [("C1", 1024), ("C4", 65536)])
-def test_single_rank_nccl_equals_direct(cfg, K):
+@pytest.mark.parametrize("cfg,K,lam", [("C1", 1024, None), ("C4", 65536, None), ("C4", 65536 + 256, 30.0)])
+def test_single_rank_nccl_equals_direct(cfg, K, lam):
+    """The in-library NCCL step (MIN key, combine / reduction against the all-reduced key, SUM of
+    [eta, A]) equals the direct single-GPU step bit for bit; at C4 sizes both run the fused
+    reduction (lambda = 30: many CTAs carry weight, so the per-CTA rescaling is exercised)."""
     w = get(cfg)
+    if lam is not None:
+        w.lam = lam
     a = from_workload(w, K=K)
     b = from_workload(w, K=K)
     b.attach_nccl()
@@ -29,6 +34,9 @@ def test_single_rank_nccl_equals_direct(cfg, K):
         b.optimize(w.x0, Ub, w.seed, i)
     torch.cuda.synchronize()
     assert torch.equal(Ua, Ub)
+    if K >= 65536:
+        assert any("epi_combine" in n for n in a.last_kernels())
+        assert any("epi_combine" in n for n in b.last_kernels())
     sa, sb = a.stats(), b.stats()
     assert sa["k_star"] == sb["k_star"] and sa["s_min"] == sb["s_min"] and sa["eta"] == sb["eta"]
     Uh = np.ascontiguousarray(w.U0.copy())
