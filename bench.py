@@ -258,12 +258,17 @@ def lscpu_model():
 
 
 # ----------------------------------------------------------------------------- reference arm
+def workload_name(cfg, w, K):
+    return "%s: %s K=%d T=%d m=%d nu=%g lambda=%g (K/N per GPU)" % (cfg, w.plant, K, w.T, w.m, w.nu, w.lam)
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle timed on the host cores, same metric/config."""
     if rank != 0:
         return 0
     from mppi_inputs import get
     w = get(args.config)
+    w.K = args.K or w.K
     ksamp = min(w.K, 1 << 14)
     for _ in range(args.warmup):
         cpu_baseline(w, steps=1, k_sample=min(ksamp, 1024))
@@ -272,8 +277,11 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * r["seconds"] / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "%s (oracle sample K=%d per step)" % (w.name, ksamp),
-                       "plant": w.plant, "K": w.K, "T": w.T},
+            # the GPU arm's workload (same string and sizes); the oracle times a bounded sample
+            # of it per step, stated in cpu_baseline.sample
+            "config": {"workload": workload_name(args.config, w, w.K), "K": w.K, "T": w.T,
+                       "n_obstacles": int(len(w.obstacles)) if w.obstacles is not None else 0,
+                       "oracle_sample_K_per_step": ksamp},
             "impl": "reference",
             "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
                              "sample": r["sample"], "cpu": lscpu_model()},
@@ -687,8 +695,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded Philox noise, committed 4 m cylinder forest, paper cost weights)",
-        "config": {"workload": "%s: %s K=%d T=%d m=%d nu=%g lambda=%g (K/N per GPU)"
-                   % (args.config, w.plant, K, w.T, w.m, w.nu, w.lam),
+        "config": {"workload": workload_name(args.config, w, K),
                    "K": K, "K_per_gpu": K_loc, "T": w.T, "n_obstacles": int(len(w.obstacles)),
                    "l2": "inputs larger than L2 (noise %.1f GB per GPU per step)" % (eps_bytes / 1e9),
                    "parallelism": "K-sharded dp%d, %s" % (world, "single GPU" if world == 1 else
