@@ -131,6 +131,7 @@ struct Ctx {
     double* d_fk = nullptr;         // Feynman-Kac partial sums (lazy)
     // NEXT-1 per-timestep cost-to-go weighting (lazy workspace)
     bool ctg = false;
+    bool ctg_fused = false;         // the last rollout launch ran the fused cost-to-go pass
     float* d_ctg = nullptr;         // [T][K_loc] q~ then S~_{t,k}
     float* d_ctg_partmin = nullptr; // [T][ceil(K_loc/256)]
     float* d_ctg_smin = nullptr;    // [T]

@@ -174,6 +174,8 @@ struct RolloutArgs {
     float cell_ox, cell_oy, cell_inv_h, cell_band;
     // fused reduction (EPI): per-CTA [A_c[T][M], m_c, eta_c, pad, pad] against the CTA's minimum
     float* epi_part;
+    // fused cost-to-go pass (QSTEP && EPI): per-t CTA minima of S~_{t,k}, [T][gridDim.x]
+    float* ctg_partmin;
     float lambda;
     // fused noise (GEN kernels): eps[t][k] drawn in-kernel with the K1 counters and written here
     float* eps_out;
@@ -664,7 +666,50 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
         if (tid == 0 && v != LLONG_MAX) atomicMin(a.min_key, v);
         if (tid == 0) sBlockKey = v;
     }
-    if constexpr (EPI) {
+    if constexpr (QSTEP && EPI) {
+        // fused cost-to-go pass (NEXT-1): ctg_kernel's arithmetic on this CTA's 256 samples --
+        // each thread suffix-sums the q~ rows of its own two samples (it wrote them: program
+        // order makes them visible), stores S~_{t,k} (non-finite -> penalty) in place and the
+        // per-t CTA minimum goes to ctg_partmin[t][blockIdx.x]; ctg_min_kernel finishes S_min,t.
+        // Same per-lane operations and order as ctg_kernel: bit-identical S~ and minima.
+        constexpr int NW = kRolloutThreads / 32;
+        const int lane = tid & 31, warp = tid >> 5;
+        float* wmin_t = reinterpret_cast<float*>(smem4);   // [NW][T]: the staged records are dead
+        const bool valid = k < a.K_loc;                     // (past the __syncthreads above)
+        float2 sacc = make_float2(0.0f, 0.0f);
+        constexpr int B = 8;                                // rows loaded ahead of the serial chain
+        for (int t1 = a.T - 1; t1 >= 0; t1 -= B) {
+            float2 q[B];
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+                q[i] = (valid && t1 - i >= 0) ? *reinterpret_cast<const float2*>(a.qstep + (size_t)(t1 - i) * a.K_loc + k)
+                                              : make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                const int t = t1 - i;
+                if (t < 0) break;
+                float v = INFINITY;
+                if (valid) {
+                    sacc = __fadd2_rn(sacc, q[i]);
+                    const float va = isfinite(sacc.x) ? sacc.x : a.penalty;
+                    const float vb2 = isfinite(sacc.y) ? sacc.y : a.penalty;
+                    *reinterpret_cast<float2*>(a.qstep + (size_t)t * a.K_loc + k) = make_float2(va, vb2);
+                    v = fminf(va, vb2);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+                if (lane == 0) wmin_t[warp * a.T + t] = v;
+            }
+        }
+        __syncthreads();
+        for (int t = tid; t < a.T; t += blockDim.x) {
+            float v = wmin_t[t];
+#pragma unroll
+            for (int w2 = 1; w2 < NW; ++w2) v = fminf(v, wmin_t[w2 * a.T + t]);
+            a.ctg_partmin[(size_t)t * gridDim.x + blockIdx.x] = v;
+        }
+    }
+    if constexpr (EPI && !QSTEP) {
         constexpr int NW = kRolloutThreads / 32;
         __shared__ float sW[2 * kRolloutThreads];
         __shared__ float sEta[NW];
@@ -1441,6 +1486,10 @@ __global__ void __launch_bounds__(1024) finalize_ctg_kernel(const FinalizeCtgArg
 
 cudaError_t launch_ctg(Ctx& c) {
     const int nblk = (int)((c.K_loc + 255) / 256);
+    if (c.ctg_fused) {   // the packed rollout already wrote S~ and the per-CTA minima
+        CtgMinArgs m{c.d_ctg_partmin, nblk, c.d_ctg_smin};
+        return emit(c, (const void*)ctg_min_kernel, dim3(c.T), dim3(256), 0, &m, sizeof(m), MPPI_KERNEL_WSUM);
+    }
     CtgArgs a{};
     a.ctg = c.d_ctg;
     a.partmin = c.d_ctg_partmin;
@@ -1807,7 +1856,11 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     const void* kern;
     if constexpr (X2 && !DIAG) {   // general Sigma / A_t: grid path only
         static_assert(NP == kCellGrid, "packed general-Sigma kernel: candidate-grid path only");
-        if (c.ctg) {
+        if (c.ctg && c.gen_eps && c.epi) {   // + fused cost-to-go pass
+            a.ctg_partmin = c.d_ctg_partmin;
+            c.ctg_fused = true;
+            kern = (const void*)rollout_kernel_x2<NP, true, true, false, true>;
+        } else if (c.ctg) {
             kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true, true, false> : (const void*)rollout_kernel_x2<NP, false, true, false>;
         } else if (c.epi_active && c.gen_eps) {   // fused reduction (EPI): the same sum of eps
             a.epi_part = c.d_epi;
@@ -1820,6 +1873,14 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
         if (c.ctg) {
             if constexpr (NP >= 0) {
                 return launch_rollout_t<Plant, DIAG, -1, true>(c, P, x0, U, eps, costs_out);
+            } else if constexpr (NP == kCellGrid) {
+                if (c.gen_eps && c.epi) {   // + fused cost-to-go pass
+                    a.ctg_partmin = c.d_ctg_partmin;
+                    c.ctg_fused = true;
+                    kern = (const void*)rollout_kernel_x2<NP, true, true, true, true>;
+                } else {
+                    kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true, true> : (const void*)rollout_kernel_x2<NP, false, true>;
+                }
             } else {
                 kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true, true> : (const void*)rollout_kernel_x2<NP, false, true>;
             }
@@ -1971,6 +2032,7 @@ bool fused_noise_applies(const Ctx& c) {
 
 cudaError_t launch_rollout(Ctx& c, const float* x0, const float* U, const float* eps,
                            float* costs_out) {
+    c.ctg_fused = false;   // set by the dispatch when the packed cost-to-go rollout runs the pass
     switch (c.plant) {
         case MPPI_PLANT_CARTPOLE:
             return launch_rollout_p<Cartpole>(c, c.params.cartpole, x0, U, eps, costs_out);

@@ -63,3 +63,33 @@ def test_u0_matches_trajectory_weighting():
     Uc = torch.tensor(w.U0, device="cuda")
     b.optimize(w.x0, Uc, 2, 0)
     assert torch.equal(Uc, Ua)
+
+
+@pytest.mark.parametrize("K,sampling", [(65536 + 4, "diag"), (1 << 17, "diag"), (65536 + 4, "A_t")])
+def test_fused_cost_to_go_pass_is_bitwise(K, sampling):
+    """The packed rollout's fused cost-to-go pass (suffix sums of each thread's own q~ rows, per-t
+    CTA minima) gives bit for bit the separate ctg_kernel's S~_{t,k}, S_min,t and update: ragged
+    last CTA, diagonal Sigma and per-step transforms A_t."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get("C4")
+    ms = [from_workload(w, K=K) for _ in range(2)]
+    ms[1].set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
+    if sampling == "A_t":
+        rng = np.random.default_rng(5)
+        At = np.array([rng.normal(size=(w.m, w.m)) * 0.2 + 1.2 * np.eye(w.m) for _ in range(w.T)])
+    for m in ms:
+        m.set_weighting(True)
+        if sampling == "A_t":
+            m.set_sampling_transform(At)
+    Us = [torch.tensor(w.U0, device="cuda") for _ in ms]
+    for i in range(2):
+        for m, U in zip(ms, Us):
+            m.optimize(w.x0, U, 9, i)
+        ka, kb = ms[0].last_kernels(), ms[1].last_kernels()
+        # mangled names: "10ctg_kernel" is the separate suffix-sum kernel
+        assert not any("10ctg_kernel" in n for n in ka) and any("ctg_min_kernel" in n for n in ka), ka
+        assert any("10ctg_kernel" in n for n in kb), kb
+        assert torch.equal(ms[0].cost_to_go(), ms[1].cost_to_go())
+        assert torch.equal(Us[0], Us[1])
+    for m in ms:
+        m.close()
