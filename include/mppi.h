@@ -309,9 +309,10 @@ typedef enum {
                                           rollouts; a small kernel rescales the partials by
                                           exp(-(m_c - S_min)/lambda) in CTA order.  Costs, noise and
                                           k* identical; U equal up to rounding.  With cost-to-go
-                                          weights the same kernels run the suffix-sum pass (S~_{t,k}
-                                          and the per-t CTA minima) in their epilogue instead of a
-                                          separate kernel: bit-identical (default 1) */
+                                          weights the same kernels run the suffix-sum pass (S~_{t,k},
+                                          bit-identical to the separate pass, and the per-t CTA
+                                          minima) and the per-(CTA, t) weighted sums in their
+                                          epilogue, rescaled to S_min,t afterwards (default 1) */
 } mppi_option_t;
 
 /* mppi_set_option — execution options that never change results (FUSED_REDUCTION: U to rounding). */

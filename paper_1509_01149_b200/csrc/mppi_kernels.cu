@@ -707,6 +707,57 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
 #pragma unroll
             for (int w2 = 1; w2 < NW; ++w2) v = fminf(v, wmin_t[w2 * a.T + t]);
             a.ctg_partmin[(size_t)t * gridDim.x + blockIdx.x] = v;
+            wmin_t[t] = v;                                  // m_{c,t} (only this thread reads column t)
+        }
+        __syncthreads();                                    // S~ rows of the whole CTA + m_{c,t}
+        // fused cost-to-go reduction: per row t, w_{t,k} = exp((S~_{t,k} - m_{c,t}) (-1/lambda))
+        // against the CTA's own per-t minimum, A_c[t][j] = sum_k w eps[t][k][j], eta_c[t] = sum_k w;
+        // epi_combine_ctg_kernel rescales by exp((m_{c,t} - S_min,t) (-1/lambda)).  Warps take
+        // rows, lanes 8 samples each (loads predicated, all in flight), as the trajectory epilogue.
+        const int k0 = 2 * blockIdx.x * blockDim.x;
+        const int nk = min(2 * (int)blockDim.x, a.K_loc - k0);
+        float* part = a.epi_part + (size_t)blockIdx.x * ((size_t)a.T * (M + 2));   // [A (T M)][eta (T)][m (T)]
+        const float* eps_src = GEN ? a.eps_out : a.eps;
+        constexpr int J = 2 * kRolloutThreads / 32;
+        for (int t = warp; t < a.T; t += NW) {
+            const float mct = wmin_t[t];
+            const float* srow = a.qstep + (size_t)t * a.K_loc + k0;
+            const float4* row4 = reinterpret_cast<const float4*>(eps_src + ((size_t)t * a.K_loc + k0) * M);
+            float sv[J];
+            float4 e[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int s2 = lane + 32 * j;
+                sv[j] = s2 < nk ? srow[s2] : INFINITY;
+                e[j] = s2 < nk ? __ldcs(row4 + s2) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            }
+            float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            float wsum = 0.0f;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const float w = lane + 32 * j < nk ? expf(__fmul_rn(sv[j] - mct, a.lambda)) : 0.0f;
+                acc.x = fmaf(w, e[j].x, acc.x);
+                acc.y = fmaf(w, e[j].y, acc.y);
+                acc.z = fmaf(w, e[j].z, acc.z);
+                acc.w = fmaf(w, e[j].w, acc.w);
+                wsum += w;
+            }
+            const bool up = lane & 16, up2 = lane & 8;
+            float c0 = up ? acc.z : acc.x, c1 = up ? acc.w : acc.y;
+            c0 += __shfl_xor_sync(0xffffffffu, up ? acc.x : acc.z, 16);
+            c1 += __shfl_xor_sync(0xffffffffu, up ? acc.y : acc.w, 16);
+            float kk = up2 ? c1 : c0;
+            kk += __shfl_xor_sync(0xffffffffu, up2 ? c0 : c1, 8);
+            kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+            kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+            kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+            if ((lane & 7) == 0) part[t * M + (lane >> 3)] = kk;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+            if (lane == 0) {
+                part[(size_t)a.T * M + t] = wsum;
+                part[(size_t)a.T * (M + 1) + t] = mct;
+            }
         }
     }
     if constexpr (EPI && !QSTEP) {
@@ -827,6 +878,40 @@ __global__ void __launch_bounds__(256) epi_combine_kernel(const EpiCombineArgs a
     for (int c = c0; c < c1; ++c) acc = fmaf(sc[c - c0], __ldg(a.epi_part + (size_t)c * stride + idx), acc);
     if (o < a.TM) a.part[(size_t)chunk * a.TM + o] = acc;
     else a.eta_part[chunk] = acc;
+}
+
+// cost-to-go version: per-(CTA, t) partials [A (T M)][eta (T)][m (T)] of the fused epilogue,
+// rescaled by exp((m_{c,t} - S_min,t) (-1/lambda)) and summed in CTA order within chunks of cpc
+// CTAs into wsum_ctg's layout: part [chunk][T][M], eta_part [chunk][T].
+struct EpiCombineCtgArgs {
+    const float* epi_part;   // [nblk][T (M + 2)]
+    const float* smin;       // [T]
+    float* part;             // [n_chunks][T][M]
+    float* eta_part;         // [n_chunks][T]
+    int nblk, cpc, T;
+    float neg_inv_lambda;
+};
+
+__global__ void __launch_bounds__(256) epi_combine_ctg_kernel(const EpiCombineCtgArgs a) {
+    pdl_wait();
+    constexpr int M = 4;
+    const int chunk = blockIdx.x;
+    const int t = blockIdx.y * blockDim.x + threadIdx.x;
+    if (t >= a.T) return;
+    const int c0 = chunk * a.cpc, c1 = min(a.nblk, c0 + a.cpc);
+    const size_t stride = (size_t)a.T * (M + 2);
+    const float sm = a.smin[t];
+    float acc[M] = {0.0f, 0.0f, 0.0f, 0.0f}, eta = 0.0f;
+    for (int c = c0; c < c1; ++c) {
+        const float* p = a.epi_part + (size_t)c * stride;
+        const float f = expf(__fmul_rn(__ldg(p + (size_t)a.T * (M + 1) + t) - sm, a.neg_inv_lambda));
+#pragma unroll
+        for (int j = 0; j < M; ++j) acc[j] = fmaf(f, __ldg(p + (size_t)t * M + j), acc[j]);
+        eta = fmaf(f, __ldg(p + (size_t)a.T * M + t), eta);
+    }
+#pragma unroll
+    for (int j = 0; j < M; ++j) a.part[((size_t)chunk * a.T + t) * M + j] = acc[j];
+    a.eta_part[(size_t)chunk * a.T + t] = eta;
 }
 
 // ------------------------------------------------------------------------------ K3 weights + GEMV
@@ -1509,6 +1594,19 @@ cudaError_t launch_ctg(Ctx& c) {
 }
 
 cudaError_t launch_wsum_ctg(Ctx& c, const float* eps) {
+    if (c.ctg_fused) {   // the rollout formed per-(CTA, t) sums: rescale to S_min,t and chunk them
+        EpiCombineCtgArgs e{};
+        e.epi_part = c.d_epi;
+        e.smin = c.d_ctg_smin;
+        e.part = c.d_part;
+        e.eta_part = c.d_ctg_eta;
+        e.nblk = c.epi_nblk;
+        e.cpc = (c.epi_nblk + c.n_chunks - 1) / c.n_chunks;
+        e.T = c.T;
+        e.neg_inv_lambda = (float)(-1.0 / (double)c.lambda);
+        const dim3 grid((unsigned)c.n_chunks, (unsigned)((c.T + 255) / 256));
+        return emit(c, (const void*)epi_combine_ctg_kernel, grid, dim3(256), 0, &e, sizeof(e), MPPI_KERNEL_WSUM);
+    }
     WsumCtgArgs a{};
     a.eps = eps;
     a.ctg = c.d_ctg;
@@ -1856,8 +1954,10 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     const void* kern;
     if constexpr (X2 && !DIAG) {   // general Sigma / A_t: grid path only
         static_assert(NP == kCellGrid, "packed general-Sigma kernel: candidate-grid path only");
-        if (c.ctg && c.gen_eps && c.epi) {   // + fused cost-to-go pass
+        if (c.ctg && c.gen_eps && c.epi && c.d_epi) {   // + fused cost-to-go pass and reduction
             a.ctg_partmin = c.d_ctg_partmin;
+            a.epi_part = c.d_epi;
+            a.lambda = (float)(-1.0 / (double)c.lambda);   // the epilogue's weights: (S - m) (-1/lambda)
             c.ctg_fused = true;
             kern = (const void*)rollout_kernel_x2<NP, true, true, false, true>;
         } else if (c.ctg) {
@@ -1874,8 +1974,10 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
             if constexpr (NP >= 0) {
                 return launch_rollout_t<Plant, DIAG, -1, true>(c, P, x0, U, eps, costs_out);
             } else if constexpr (NP == kCellGrid) {
-                if (c.gen_eps && c.epi) {   // + fused cost-to-go pass
+                if (c.gen_eps && c.epi && c.d_epi) {   // + fused cost-to-go pass and reduction
                     a.ctg_partmin = c.d_ctg_partmin;
+                    a.epi_part = c.d_epi;
+                    a.lambda = (float)(-1.0 / (double)c.lambda);   // (S - m) (-1/lambda)
                     c.ctg_fused = true;
                     kern = (const void*)rollout_kernel_x2<NP, true, true, true, true>;
                 } else {

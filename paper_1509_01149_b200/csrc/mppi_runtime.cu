@@ -509,7 +509,8 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
         (a = dalloc(c, &c.d_U, (size_t)T * m, "U staging")) ||
         (a = dalloc(c, &c.d_obs, (size_t)(c.n_obs_pairs > 0 ? c.n_obs_pairs : 1), "obstacles")) ||
         (a = dalloc(c, &c.d_flags, (size_t)((ncols + kWsumThreads - 1) / kWsumThreads), "weight block flags")) ||
-        (c.epi_nblk > 0 && (a = dalloc(c, &c.d_epi, (size_t)c.epi_nblk * ((size_t)T * m + 4), "fused-reduction partials"))) ||
+        (c.epi_nblk > 0 && (a = dalloc(c, &c.d_epi, (size_t)c.epi_nblk * ((size_t)T * m + std::max<size_t>(4, 2 * (size_t)T)),
+                                         "fused-reduction partials"))) ||   // trajectory: T m + 4; cost-to-go: T (m + 2)
         (!c.cells_host.empty() &&
          ((a = dalloc(c, &c.d_cells, c.cells_host.size(), "obstacle grid")) ||
           (a = dalloc(c, &c.d_cent, c.cent_host.size(), "obstacle centres"))))) {

@@ -65,13 +65,18 @@ def test_u0_matches_trajectory_weighting():
     assert torch.equal(Uc, Ua)
 
 
-@pytest.mark.parametrize("K,sampling", [(65536 + 4, "diag"), (1 << 17, "diag"), (65536 + 4, "A_t")])
-def test_fused_cost_to_go_pass_is_bitwise(K, sampling):
+@pytest.mark.parametrize("K,sampling,lam", [(65536 + 4, "diag", None), (1 << 17, "diag", 500.0),
+                                             (65536 + 4, "A_t", 500.0)])
+def test_fused_cost_to_go_pass_is_bitwise(K, sampling, lam):
     """The packed rollout's fused cost-to-go pass (suffix sums of each thread's own q~ rows, per-t
-    CTA minima) gives bit for bit the separate ctg_kernel's S~_{t,k}, S_min,t and update: ragged
-    last CTA, diagonal Sigma and per-step transforms A_t."""
+    CTA minima) gives bit for bit the separate ctg_kernel's S~_{t,k}; its fused reduction (weights
+    against the per-(CTA, t) minima, rescaled by epi_combine_ctg_kernel) gives the separate
+    reduction's update to rounding: ragged last CTA, diagonal Sigma and per-step transforms A_t,
+    one-hot (config lambda) and dense (lambda = 500) weights."""
     from paper_1509_01149_b200 import _capi as A
     w = get("C4")
+    if lam is not None:
+        w.lam = lam
     ms = [from_workload(w, K=K) for _ in range(2)]
     ms[1].set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
     if sampling == "A_t":
@@ -88,8 +93,10 @@ def test_fused_cost_to_go_pass_is_bitwise(K, sampling):
         ka, kb = ms[0].last_kernels(), ms[1].last_kernels()
         # mangled names: "10ctg_kernel" is the separate suffix-sum kernel
         assert not any("10ctg_kernel" in n for n in ka) and any("ctg_min_kernel" in n for n in ka), ka
-        assert any("10ctg_kernel" in n for n in kb), kb
+        assert any("epi_combine_ctg" in n for n in ka) and not any("wsum_ctg" in n for n in ka), ka
+        assert any("10ctg_kernel" in n for n in kb) and any("wsum_ctg" in n for n in kb), kb
         assert torch.equal(ms[0].cost_to_go(), ms[1].cost_to_go())
-        assert torch.equal(Us[0], Us[1])
+        torch.testing.assert_close(Us[0], Us[1], rtol=1e-5, atol=1e-6)
+        Us[1].copy_(Us[0])
     for m in ms:
         m.close()
