@@ -745,3 +745,30 @@ def test_closed_loop_c2_swings_up_like_the_oracle(oracle):
         first = int(np.argmax(series < 0.05))
         assert series.min() < 0.05 and first < 100
         assert cost[-50:].mean() < 50.0
+
+
+@pytest.mark.parametrize("weighting", ["trajectory", "cost_to_go"])
+def test_fused_reduction_long_horizon(weighting):
+    """T = 1000 with the obstacle grid still in shared memory: the fused epilogues (trajectory
+    and cost-to-go) against the separate kernels -- costs / cost-to-go bitwise, U to rounding."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get("C4", T=1000)
+    w.lam = 30.0
+    a = from_workload(w, K=65536 + 4)
+    b = from_workload(w, K=65536 + 4)
+    b.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
+    if weighting == "cost_to_go":
+        a.set_weighting(True)
+        b.set_weighting(True)
+    Ua, Ub = cuda_u(w), cuda_u(w)
+    a.optimize(w.x0, Ua, 2, 0)
+    b.optimize(w.x0, Ub, 2, 0)
+    ka = a.last_kernels()
+    assert any("epi_combine" in n for n in ka), ka
+    assert a.stats()["k_star"] == b.stats()["k_star"]
+    if weighting == "cost_to_go":
+        assert torch.equal(a.cost_to_go(), b.cost_to_go())
+    assert torch.isfinite(Ua).all()
+    torch.testing.assert_close(Ua, Ub, rtol=1e-5, atol=1e-6)
+    a.close()
+    b.close()
