@@ -434,7 +434,10 @@ mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed,
  * V(x0) = -lambda log Psi(x0) is the value function of PAPER.md:56.
  *   x0  : HOST float [n];  seed, step : as mppi_optimize.
  *   out : HOST double [3] = {log_psi, se_log_psi, s_min}.
- * SYNCHRONOUS.  world == 1 only (else UNSUPPORTED); nu != 1 -> UNSUPPORTED. */
+ * Sharded (world > 1, after mppi_nccl_attach): every rank rolls out its K/G samples, an NCCL
+ * MIN of the (cost, k) key gives the global S_min, an NCCL SUM adds the fp64 partial sums, and
+ * every rank returns the same estimate over all K samples.
+ * SYNCHRONOUS.  world > 1 without a communicator -> UNSUPPORTED; nu != 1 -> UNSUPPORTED. */
 mppi_status_t mppi_feynman_kac(mppi_ctx* ctx, const float* x0, uint64_t seed, uint64_t step,
                                double* out);
 

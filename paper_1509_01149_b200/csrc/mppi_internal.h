@@ -196,6 +196,7 @@ const char* nccl_error(int r);
 int nccl_min_key(Ctx& c, long long* key);
 int nccl_min_f32(Ctx& c, float* buf, size_t count);
 int nccl_sum_buf(Ctx& c, float* buf, size_t count);
+int nccl_sum_f64(Ctx& c, double* buf, size_t count);
 cudaError_t launch_fk_reduce(Ctx& c, double* part, int nblk);   // Feynman-Kac partial sums
 cudaError_t launch_ctg(Ctx& c);                                  // cost-to-go + per-t minima
 cudaError_t launch_wsum_ctg(Ctx& c, const float* eps);

@@ -89,4 +89,8 @@ int nccl_sum_buf(Ctx& c, float* buf, size_t count) {
     return (int)api().all_reduce(buf, buf, count, ncclFloat32, ncclSum, (ncclComm_t)c.nccl, c.stream);
 }
 
+int nccl_sum_f64(Ctx& c, double* buf, size_t count) {
+    return (int)api().all_reduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)c.nccl, c.stream);
+}
+
 }  // namespace mppi

@@ -1088,7 +1088,8 @@ mppi_status_t mppi_feynman_kac(mppi_ctx* ctx, const float* x0, uint64_t seed, ui
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
     if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
-    if (c.world != 1) return fail(MPPI_ERR_UNSUPPORTED, "mppi_feynman_kac needs world == 1");
+    if (c.world != 1 && !c.nccl)
+        return fail(MPPI_ERR_UNSUPPORTED, "mppi_feynman_kac with world > 1 needs mppi_nccl_attach");
     if (c.nu != 1.0f) return fail(MPPI_ERR_UNSUPPORTED, "mppi_feynman_kac samples the uncontrolled "
                                   "dynamics P: create the context with nu == 1");
     c.last_launches = 0;
@@ -1099,7 +1100,15 @@ mppi_status_t mppi_feynman_kac(mppi_ctx* ctx, const float* x0, uint64_t seed, ui
     if (mppi_status_t s = do_rollout(c, x0, c.d_U, seed, step, nullptr, nullptr, &eps)) return s;
     const int nblk = 148;
     if (!c.d_fk) MPPI_CUDA(cudaMalloc((void**)&c.d_fk, 2 * nblk * sizeof(double)), "fk partials");
+    if (c.nccl) {   // sharded: the global S_min, then the sums of exp(-(S - S_min)/lambda) over ranks
+        int r = nccl_min_key(c, &c.d_stats->min_key);
+        if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(MIN key): %s", nccl_error(r));
+    }
     MPPI_CUDA(launch_fk_reduce(c, c.d_fk, nblk), "fk_reduce launch");
+    if (c.nccl) {
+        int r = nccl_sum_f64(c, c.d_fk, (size_t)2 * nblk);
+        if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(SUM fk partials): %s", nccl_error(r));
+    }
     double part[2 * 148];
     long long key = 0;
     MPPI_CUDA(cudaMemcpyAsync(part, c.d_fk, sizeof(part), cudaMemcpyDeviceToHost, c.stream), "fk D2H");
@@ -1111,7 +1120,7 @@ mppi_status_t mppi_feynman_kac(mppi_ctx* ctx, const float* x0, uint64_t seed, ui
     b = b >= 0 ? b : (b ^ 0x7fffffff);
     float smin;
     memcpy(&smin, &b, sizeof(smin));
-    const double K = (double)c.K_loc;
+    const double K = (double)(c.nccl ? c.K : c.K_loc);   // the sums cover every rank's samples
     const double mean = s1 / K;
     const double var = K > 1 ? (s2 / K - mean * mean) * K / (K - 1) : 0.0;
     out[0] = -(double)smin / (double)c.lambda + log(mean);

@@ -43,3 +43,25 @@ def test_feynman_kac_requires_nu_one():
     m = MPPI("cartpole", 256, w.T, w.dt, 1.0, 2.0, w.Sigma, w.R)
     with pytest.raises(MppiError):
         m.feynman_kac(w.x0)
+
+
+def test_feynman_kac_through_nccl_equals_direct():
+    """Sharded path of mppi_feynman_kac on a single-rank communicator (one GPU per call here):
+    NCCL MIN of the key and SUM of the fp64 partials give the direct estimate bit for bit; a
+    world-2 context without a communicator is refused."""
+    from mppi_inputs import get as get_w
+    from paper_1509_01149_b200 import from_workload
+    w = get_w("C4")
+    w.nu = 1.0
+    a = from_workload(w, K=1 << 16)
+    b = from_workload(w, K=1 << 16)
+    b.attach_nccl()
+    ra = a.feynman_kac(w.x0, seed=4, step=2)
+    rb = b.feynman_kac(w.x0, seed=4, step=2)
+    assert ra == rb and np.isfinite(ra[0])
+    a.close()
+    b.close()
+    c = from_workload(w, K=1024, rank=0, world=2)
+    with pytest.raises(MppiError):
+        c.feynman_kac(w.x0)
+    c.close()
