@@ -418,7 +418,11 @@ mppi_status_t mppi_cost_to_go(mppi_ctx* ctx, float* out);
  *   reset_crash : nonzero clears the device plant's crash flag (quadrotor) first.
  *   x_log  : DEVICE float [n_steps + 1][n] (x_0 .. x_N) or NULL;  u_log: DEVICE [n_steps][m] (the
  *            executed u_0) or NULL;  q_log: DEVICE [n_steps] (q(x_{i+1})) or NULL.
- * SYNCHRONOUS (returns after the loop ran).  world == 1 and plant != LINEAR, else UNSUPPORTED. */
+ * Sharded (world > 1, after mppi_nccl_attach): each step runs with the library's collectives and
+ * every rank advances its own replica of the plant with the same all-reduced u_0 (enqueued step by
+ * step instead of one graph).
+ * SYNCHRONOUS (returns after the loop ran).  plant != LINEAR, and world == 1 or a communicator,
+ * else UNSUPPORTED. */
 mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed, uint64_t step0,
                                int32_t n_steps, const float* u_init, int32_t reset_crash,
                                float* x_log, float* u_log, float* q_log);

@@ -349,7 +349,8 @@ mppi_status_t sticky_check(Ctx& c) {
 mppi_status_t do_rollout(Ctx& c, const float* x0, const float* U, uint64_t seed, uint64_t step,
                          const float* noise, float* costs_out, const float** eps_used) {
     if (!x0 || !U) return fail(MPPI_ERR_INVALID_ARG, "x0 and U must be non-NULL");
-    if (!all_finite(x0, c.n)) return fail(MPPI_ERR_INVALID_ARG, "x0 must be finite");
+    // (a device-resident x0 -- the closed loop's plant state -- is not readable here)
+    if (!c.x0_on_device && !all_finite(x0, c.n)) return fail(MPPI_ERR_INVALID_ARG, "x0 must be finite");
     mppi_status_t s = sticky_check(c);
     if (s) return s;
     const float* eps = noise;
@@ -1038,13 +1039,34 @@ mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed,
                                float* x_log, float* u_log, float* q_log) {
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
-    if (c.world != 1) return fail(MPPI_ERR_UNSUPPORTED, "mppi_closed_loop needs world == 1");
+    if (c.world != 1 && !c.nccl)
+        return fail(MPPI_ERR_UNSUPPORTED, "mppi_closed_loop with world > 1 needs mppi_nccl_attach");
     if (c.plant == MPPI_PLANT_LINEAR) return fail(MPPI_ERR_UNSUPPORTED, "mppi_closed_loop: linear test plant");
     if (!x || !U || !u_init || n_steps < 1) return fail(MPPI_ERR_INVALID_ARG, "x, U, u_init non-NULL, n_steps >= 1");
     if (!all_finite(u_init, c.m)) return fail(MPPI_ERR_INVALID_ARG, "u_init must be finite");
     if (mppi_status_t s = sticky_check(c)) return s;
     if (reset_crash)
         MPPI_CUDA(cudaMemsetAsync(&c.d_stats->plant_crashed, 0, sizeof(int), c.stream), "crash reset");
+    if (c.nccl) {
+        // sharded: every rank runs the step with the library's collectives and advances its own
+        // replica of the plant with the same (all-reduced, hence identical) u_0 -- the replicas
+        // stay bitwise equal.  Enqueued step by step (the collectives sit between the kernels).
+        if (x_log) MPPI_CUDA(cudaMemcpyAsync(x_log, x, (size_t)c.n * sizeof(float), cudaMemcpyDeviceToDevice, c.stream), "x_log[0]");
+        int launches = 0;
+        for (int i = 0; i < n_steps; ++i) {
+            c.x0_on_device = true;
+            mppi_status_t s = optimize_nccl(c, x, U, seed, step0 + (uint64_t)i, nullptr);
+            c.x0_on_device = false;
+            if (s) return s;
+            launches += c.last_launches;
+            MPPI_CUDA(launch_advance(c, x, U, u_init, x_log ? x_log + (size_t)(i + 1) * c.n : nullptr,
+                                     u_log ? u_log + (size_t)i * c.m : nullptr, q_log ? q_log + i : nullptr),
+                      "closed-loop advance");
+        }
+        c.last_launches = launches + n_steps;
+        MPPI_CUDA(cudaStreamSynchronize(c.stream), "stream sync");
+        return MPPI_OK;
+    }
     // collect n_steps x [noise, rollout (x0 from device), wsum, finalize, advance] into one graph
     c.last_launches = 0;
     c.last_funcs.clear();

@@ -77,3 +77,29 @@ def test_fig1_trend_cost_falls_with_nu():
     v = [mean_cost[nu] for nu in (1.0, 10.0, 100.0, 1000.0)]
     assert v == sorted(v, reverse=True), mean_cost
     assert v[0] > 2 * v[-1]
+
+
+@pytest.mark.parametrize("cfg,K", [("C2", 4096), ("C4", 65536)])
+def test_sharded_closed_loop_single_rank_equals_graph_loop(cfg, K):
+    """mppi_closed_loop through the library's communicator (single-rank: one GPU per call here)
+    steps the same states and controls as the single-GPU graph loop -- bit for bit at C2; at C4
+    size the sharded step runs the fused noise and reduction (the graph loop draws the noise in
+    a separate pass and reduces with K3), so the controls agree to rounding."""
+    w = get(cfg)
+    a = from_workload(w, K=K)
+    b = from_workload(w, K=K)
+    b.attach_nccl()
+    steps = 8
+    outs = []
+    for m in (a, b):
+        x = torch.tensor(w.x0, device="cuda")
+        U = torch.tensor(w.U0, device="cuda")
+        xl, ul, ql = m.closed_loop(x, U, steps, seed=w.seed, step0=3, u_init=np.zeros(w.m))
+        outs.append((xl.cpu().numpy(), ul.cpu().numpy()))
+    if K < 65536:
+        assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    else:
+        assert np.allclose(outs[0][1], outs[1][1], rtol=1e-4, atol=1e-5)
+        assert np.allclose(outs[0][0], outs[1][0], rtol=1e-4, atol=1e-5)
+    a.close()
+    b.close()
