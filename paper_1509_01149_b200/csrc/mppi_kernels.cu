@@ -902,6 +902,7 @@ __global__ void __launch_bounds__(256) epi_combine_ctg_kernel(const EpiCombineCt
     const size_t stride = (size_t)a.T * (M + 2);
     const float sm = a.smin[t];
     float acc[M] = {0.0f, 0.0f, 0.0f, 0.0f}, eta = 0.0f;
+#pragma unroll 8   // independent loads in flight (65 -> 48 us at C5)
     for (int c = c0; c < c1; ++c) {
         const float* p = a.epi_part + (size_t)c * stride;
         const float f = expf(__fmul_rn(__ldg(p + (size_t)a.T * (M + 1) + t) - sm, a.neg_inv_lambda));
