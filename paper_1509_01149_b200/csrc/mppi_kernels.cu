@@ -1264,6 +1264,7 @@ struct CtgArgs {
 };
 
 __global__ void __launch_bounds__(256) ctg_kernel(const CtgArgs a) {
+    pdl_wait();
     extern __shared__ float wmin_t[];   // [8 warps][T]
     const int k = blockIdx.x * 256 + threadIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1306,6 +1307,7 @@ struct CtgMinArgs {
 };
 
 __global__ void __launch_bounds__(256) ctg_min_kernel(const CtgMinArgs a) {
+    pdl_wait();
     const int t = blockIdx.x;
     float v = INFINITY;
     for (int i = threadIdx.x; i < a.nblk; i += 256) v = fminf(v, a.partmin[(size_t)t * a.nblk + i]);
@@ -1336,6 +1338,7 @@ struct WsumCtgArgs {
 
 template <int M>
 __global__ void __launch_bounds__(kWsumThreads) wsum_ctg_kernel(const WsumCtgArgs a) {
+    pdl_wait();
     constexpr int SPC = 4 / M;
     constexpr int TT = kWsumTT;
     const int chunk = blockIdx.x;
@@ -1408,6 +1411,7 @@ __global__ void __launch_bounds__(kWsumThreads) wsum_ctg_kernel(const WsumCtgArg
 // and the matching TT x (CW * SPC) cost-to-go values; same per-thread accumulation order.
 template <int M>
 __global__ void __launch_bounds__(kWsumThreads, 2) wsum_ctg_tma_kernel(const WsumCtgArgs a) {
+    pdl_wait();
     constexpr int SPC = 4 / M;
     constexpr int TT = kWsumTT;
     constexpr int CW = kWsumThreads;

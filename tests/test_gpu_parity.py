@@ -515,20 +515,29 @@ def test_fused_noise_rollout_is_bitwise_separate_pass(cfg, T, Ks):
 
 @pytest.mark.parametrize("cfg,K", [("C2", 4096), ("C3", 16384), ("C4", 65536)])
 def test_pdl_graph_is_bitwise_plain_graph(cfg, K):
-    """MPPI_OPTION_PDL: programmatic kernel->kernel edges change launch timing only."""
+    """MPPI_OPTION_PDL: programmatic kernel->kernel edges change launch timing only (every kernel
+    that can follow another in a step graph waits in griddepcontrol.wait): trajectory and
+    cost-to-go weights."""
     from paper_1509_01149_b200 import _capi as A
     w = get(cfg)
-    a = from_workload(w, K=K)
-    b = from_workload(w, K=K)
-    a.set_option(A.MPPI_OPTION_PDL, 1)
-    Ua, Ub = cuda_u(w), cuda_u(w)
-    for i in range(3):
-        a.optimize(w.x0, Ua, 4, i)
-        b.optimize(w.x0, Ub, 4, i)
-    torch.cuda.synchronize()
-    assert torch.equal(Ua, Ub) and a.stats() == b.stats()
-    a.close()
-    b.close()
+    for ctg in (False, True):
+        a = from_workload(w, K=K)
+        b = from_workload(w, K=K)
+        a.set_option(A.MPPI_OPTION_PDL, 1)
+        b.set_option(A.MPPI_OPTION_PDL, 0)
+        if ctg:
+            a.set_weighting(True)
+            b.set_weighting(True)
+        Ua, Ub = cuda_u(w), cuda_u(w)
+        for i in range(3):
+            a.optimize(w.x0, Ua, 4, i)
+            b.optimize(w.x0, Ub, 4, i)
+        torch.cuda.synchronize()
+        assert torch.equal(Ua, Ub) and a.stats() == b.stats()
+        if ctg:
+            assert torch.equal(a.cost_to_go(), b.cost_to_go())
+        a.close()
+        b.close()
 
 
 @pytest.mark.parametrize("cfg,K", [("C4", 65536 + 4), ("C3", 1 << 16), ("C2", (1 << 17) + 8)])
