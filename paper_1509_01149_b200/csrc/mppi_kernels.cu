@@ -271,9 +271,11 @@ struct ScalarRollout {
             }
             float duGdu = 0.0f, uRdu = 0.0f;
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
+            for (int i = 0; i < M; ++i) {   // du'G du over the staged upper triangle
+                float in = du[i] * G[i * M + i];
 #pragma unroll
-                for (int j = 0; j < M; ++j) duGdu = fmaf(du[i] * G[i * M + j], du[j], duGdu);
+                for (int j = i + 1; j < M; ++j) in = fmaf(G[i * M + j], du[j], in);
+                duGdu = fmaf(du[i], in, duGdu);
                 uRdu = fmaf(bb[i], du[i], uRdu);
             }
             is = duGdu + (uRdu + is);
@@ -328,8 +330,13 @@ __device__ __forceinline__ void stage_step_constants(const RolloutArgs<PP>& a, f
     if (!DIAG) {
         for (int o = tid; o < a.T * 2 * M * M; o += blockDim.x) {
             const int t = o / (2 * M * M), r = o % (2 * M * M), which = r / (M * M), ij = r % (M * M);
-            // default transform A = sqrt(nu) I: F = sqrt(nu) L, G = (1 - 1/nu)/2 R
-            sMat[o] = a.mats ? a.mats[t * 32 + which * 16 + ij] : (which == 0 ? a.sL[ij] : a.c1 * a.R[ij]);
+            // default transform A = sqrt(nu) I: F = sqrt(nu) L, G = (1 - 1/nu)/2 R.  G is staged for
+            // the quadratic form du'G du = sum_i du_i (G_ii du_i + sum_{j>i} (G_ij + G_ji) du_j):
+            // its strict upper triangle holds G_ij + G_ji (the lower one is not read)
+            auto g = [&](int q) { return a.mats ? a.mats[t * 32 + 16 + q] : a.c1 * a.R[q]; };
+            const int i = ij / M, j = ij % M;
+            sMat[o] = which == 0 ? (a.mats ? a.mats[t * 32 + ij] : a.sL[ij])
+                                 : (j > i ? g(i * M + j) + g(j * M + i) : g(ij));
         }
     }
     for (int t = tid; t < a.T; t += blockDim.x) {
@@ -575,9 +582,11 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
                 }
                 V2 duGdu = vb(0.0f), uRdu = vb(0.0f);
 #pragma unroll
-                for (int i = 0; i < M; ++i) {
+                for (int i = 0; i < M; ++i) {   // du'G du over the staged upper triangle (as above)
+                    V2 in = du[i] * vb(G[i * M + i]);
 #pragma unroll
-                    for (int j = 0; j < M; ++j) duGdu = fma2(du[i] * vb(G[i * M + j]), du[j], duGdu);
+                    for (int j = i + 1; j < M; ++j) in = fma2(vb(G[i * M + j]), du[j], in);
+                    duGdu = fma2(du[i], in, duGdu);
                     uRdu = fma2(vb(bb[i]), du[i], uRdu);
                 }
                 is = duGdu + (uRdu + is);
