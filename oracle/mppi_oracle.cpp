@@ -573,6 +573,15 @@ void oracle_bm_angle(uint32_t w, float* s, float* c) { bm_angle(w, s, c); }
 
 void oracle_bm_normals(const uint32_t* w, float* z) { bm_normals(w, z); }
 
+// The same two functions over arrays of input words (for the exhaustive GPU comparison).
+void oracle_bm_radius_words(const uint32_t* w, int64_t n, float* r) {
+    for (int64_t i = 0; i < n; ++i) r[i] = bm_radius(w[i]);
+}
+
+void oracle_bm_angle_words(const uint32_t* w, int64_t n, float* s, float* c) {
+    for (int64_t i = 0; i < n; ++i) bm_angle(w[i], &s[i], &c[i]);
+}
+
 // Exhaustive BM32 accuracy sweep (pin P2).  Over all 2^23 radius inputs: max ulp error
 // of ln u1 and of r against fp64 libm; over all 2^24 angles: max |sin err|, |cos err|.
 void oracle_bm_accuracy(double* max_ln_ulp, double* max_r_ulp, double* max_sin_err,

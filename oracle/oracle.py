@@ -80,6 +80,8 @@ def lib():
         L.oracle_bm_radius.restype = C.c_float
         L.oracle_bm_angle.argtypes = [C.c_uint32, fp, fp]
         L.oracle_bm_normals.argtypes = [up, fp]
+        L.oracle_bm_radius_words.argtypes = [up, C.c_int64, fp]
+        L.oracle_bm_angle_words.argtypes = [up, C.c_int64, fp, fp]
         L.oracle_bm_accuracy.argtypes = [dp] * 5
         L.oracle_noise.argtypes = [C.c_uint64, C.c_uint64, C.c_int32, C.c_int64, C.c_int64,
                                    C.c_int32, fp]
@@ -159,6 +161,23 @@ def bm_normals(w):
     z = np.zeros(4, np.float32)
     lib().oracle_bm_normals(w.ctypes.data_as(C.POINTER(C.c_uint32)), _fp(z))
     return z
+
+
+def bm_radius_words(w):
+    """r(w) of Appendix B "Radius" for every word of the uint32 array w."""
+    w = np.ascontiguousarray(np.asarray(w, np.uint32))
+    r = np.empty(w.shape, np.float32)
+    lib().oracle_bm_radius_words(w.ctypes.data_as(C.POINTER(C.c_uint32)), w.size, _fp(r))
+    return r
+
+
+def bm_angle_words(w):
+    """(sin theta(w), cos theta(w)) of Appendix B "Angle" for every word of the uint32 array w."""
+    w = np.ascontiguousarray(np.asarray(w, np.uint32))
+    s = np.empty(w.shape, np.float32)
+    c = np.empty(w.shape, np.float32)
+    lib().oracle_bm_angle_words(w.ctypes.data_as(C.POINTER(C.c_uint32)), w.size, _fp(s), _fp(c))
+    return s, c
 
 
 def bm_accuracy():

@@ -15,6 +15,11 @@ KEYS = [
     "sm__inst_executed.sum", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_fma.sum", "sm__inst_executed_pipe_alu.sum", "sm__inst_executed_pipe_lsu.sum",
     "sm__inst_executed_pipe_xu.sum", "sm__inst_executed_pipe_uniform.sum",
+    "sm__inst_executed_pipe_fmaheavy.sum", "sm__inst_executed_pipe_fmalite.sum", "sm__inst_executed_pipe_adu.sum",
+    "sm__inst_executed_pipe_cbu.sum", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fmalite_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg",
     "sm__sass_thread_inst_executed_op_fadd_pred_on.sum", "sm__sass_thread_inst_executed_op_fmul_pred_on.sum",
     "sm__sass_thread_inst_executed_op_ffma_pred_on.sum", "sm__sass_thread_inst_executed_op_fadd2_pred_on.sum",
     "sm__sass_thread_inst_executed_op_fmul2_pred_on.sum", "sm__sass_thread_inst_executed_op_ffma2_pred_on.sum",
@@ -37,6 +42,14 @@ def report(path, out):
             for k in KEYS:
                 if k in idx:
                     f.write("  %-62s %22s %s\n" % (k, d[idx[k]], units[idx[k]]))
+            for k in sorted(h for h in hdr if h.startswith("smsp__average_warps_issue_stalled_")
+                            and h.endswith("_per_issue_active.ratio")):
+                try:
+                    v = float(d[idx[k]].replace(",", ""))
+                except ValueError:
+                    continue
+                if v >= 0.05:
+                    f.write("  %-62s %22.3f per issue\n" % (k[len("smsp__average_warps_issue_stalled_"):], v))
             fl = 0.0
             for k, w in (("fadd", 1), ("fmul", 1), ("ffma", 2), ("fadd2", 2), ("fmul2", 2), ("ffma2", 4)):
                 key = "sm__sass_thread_inst_executed_op_%s_pred_on.sum" % k

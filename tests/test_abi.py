@@ -42,6 +42,17 @@ def test_exports_every_declared_symbol(capi):
     assert capi.lib().mppi_abi_version() == 1
 
 
+def test_probe_library_exports_its_header():
+    """libmppi_probe.so (FP32 peak probe, BM32 sweep probe) exports what include/mppi_probe.h declares."""
+    from paper_1509_01149_b200 import probe_build
+    lib = probe_build.build()
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "mppi_probe.h")).read(), flags=re.S)
+    funcs = sorted(set(re.findall(r"\b(mppi_[a-z0-9_]+)\s*\(", src)))
+    assert funcs == ["mppi_probe_bm32", "mppi_probe_fp32"]
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True).stdout
+    assert set(funcs) <= set(re.findall(r" T (mppi_\w+)", out))
+
+
 def test_library_is_sm100a(capi):
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", capi.LIB_PATH],
                          capture_output=True, text=True).stdout

@@ -1,6 +1,7 @@
 """NEXT-2 on the GPU: Algorithm 1's receding-horizon loop on the device (mppi_closed_loop,
-PAPER.md:356-378) against the host-driven loop through the same API, plus the Fig. 1 trend
-(average running cost falls with the exploration variance nu)."""
+PAPER.md:356-378) against the fp64 oracle step by step (optimisation, device plant step, shift)
+and over the first 10 steps, against the host-driven loop through the same API, plus the Fig. 1
+trend (average running cost falls with the exploration variance nu)."""
 import math
 
 import numpy as np
@@ -103,3 +104,83 @@ def test_sharded_closed_loop_single_rank_equals_graph_loop(cfg, K):
         assert np.allclose(outs[0][0], outs[1][0], rtol=1e-4, atol=1e-5)
     a.close()
     b.close()
+
+
+# ----------------------------------------------------------------------------- against the oracle
+def _problem(oracle, w):
+    return oracle.Problem(w.plant, T=w.T, dt=w.dt, lam=w.lam, nu=w.nu, Sigma=w.Sigma, R=w.R,
+                          obstacles=w.obstacles if w.plant == "quadrotor" else None)
+
+
+@pytest.mark.parametrize("cfg,K", [("C2", 4096), ("C3", 4096), ("C4", 8192)])
+def test_device_loop_step_by_step_against_oracle(oracle, cfg, K):
+    """Each of the first 10 receding-horizon steps of mppi_closed_loop against
+    the fp64 oracle, from the device's own state and controls (so fp32/fp64 chaos cannot build
+    up):  the optimisation (decoupled U within 1e-5 on the GPU's costs and noise; coupled within
+    1e-5 whenever the A20 bound allows), the device plant step x_{i+1} = x_i + F(x_i, u_0) dt
+    (the advance kernel, :377) and q(x_{i+1}) element-wise, and the shift (:372-375) bitwise.
+    The 10-step graph loop then reproduces the step-by-step states and controls bit for bit."""
+    w = get(cfg)
+    w.K = K
+    g = from_workload(w)
+    pb = _problem(oracle, w)
+    ui = np.zeros(w.m, np.float32)
+    x = torch.tensor(w.x0, device="cuda")
+    U = torch.tensor(w.U0, device="cuda")
+    steps, crashed, coupled = 10, 0, 0
+    xs, us = [w.x0.copy()], []
+    for i in range(steps):
+        x_i = x.cpu().numpy().copy()
+        U_before = U.cpu().numpy().copy()
+        xl, ul, ql = g.closed_loop(x, U, 1, seed=w.seed, step0=i, u_init=ui, reset_crash=(i == 0))
+        xl, ul, ql = xl.cpu().numpy(), ul.cpu().numpy(), float(ql.cpu().numpy()[0])
+        U_now = U.cpu().numpy()
+        assert np.array_equal(xl[0], x_i)
+        U_after = np.concatenate([ul, U_now[:-1]], axis=0).astype(np.float64)
+        # optimisation of step i
+        costs, _ = g.rollout_costs(x_i, torch.tensor(U_before, device="cuda"), w.seed, i)
+        c = costs.cpu().numpy().astype(np.float64)
+        eps = g.noise(w.seed, i).cpu().numpy()
+        Ud = oracle.update(pb, c, eps, U_before)[0]
+        assert np.max(np.abs(U_after - Ud)) <= 1e-5, (i, np.max(np.abs(U_after - Ud)))
+        full = oracle.optimize(pb, x_i, U_before, eps)
+        wbar = full["weights"] / full["weights"].sum()
+        du = math.sqrt(w.nu) * np.einsum("ij,tkj->tki", np.linalg.cholesky(w.Sigma), eps.astype(np.float64))
+        dev = np.abs(du - np.einsum("k,tki->ti", wbar, du)[:, None, :]).max(axis=(0, 2))
+        if np.sum(wbar * np.abs(c - full["costs"]) * dev) / w.lam <= 5e-6:
+            assert np.max(np.abs(U_after - full["U"])) <= 1e-5
+            coupled += 1
+        # device plant step and its cost
+        x_ref, q_ref, crashed = oracle.plant_step(pb, x_i.astype(np.float64), ul[0].astype(np.float64), crashed)
+        scale = np.maximum(np.abs(x_ref), 1.0)
+        assert np.all(np.abs(xl[1] - x_ref) <= 1e-5 * scale), (i, np.abs(xl[1] - x_ref) / scale)
+        assert abs(ql - q_ref) <= 1e-5 * max(abs(q_ref), 1.0)
+        # shift
+        assert np.array_equal(U_now, oracle.shift(U_after.astype(np.float32), ui).astype(np.float32))
+        xs.append(xl[1].copy())
+        us.append(ul[0].copy())
+    assert coupled >= steps // 2, "coupled U check ran on %d of %d steps" % (coupled, steps)
+    # the 10-step graph loop equals the step-by-step loop
+    x = torch.tensor(w.x0, device="cuda")
+    U = torch.tensor(w.U0, device="cuda")
+    xl, ul, _ = g.closed_loop(x, U, steps, seed=w.seed, step0=0, u_init=ui)
+    assert np.array_equal(xl.cpu().numpy(), np.array(xs)) and np.array_equal(ul.cpu().numpy(), np.array(us))
+    g.close()
+
+
+@pytest.mark.parametrize("cfg,K", [("C2", 4096), ("C4", 8192)])
+def test_device_loop_tracks_oracle_closed_loop(oracle, cfg, K):
+    """The first 10 steps of the device loop against oracle.closed_loop (fp64 all the way): in the
+    argmin regime both pick the same samples, so states agree to fp32 rounding."""
+    w = get(cfg)
+    w.K = K
+    g = from_workload(w)
+    steps = 10
+    x = torch.tensor(w.x0, device="cuda")
+    U = torch.tensor(w.U0, device="cuda")
+    xl, ul, ql = g.closed_loop(x, U, steps, seed=w.seed, step0=0, u_init=np.zeros(w.m))
+    xs, qs = oracle.closed_loop(_problem(oracle, w), w.x0, w.U0, steps, w.seed, K=K)
+    xl = xl.cpu().numpy().astype(np.float64)
+    assert np.allclose(xl, xs, rtol=1e-4, atol=1e-5), np.max(np.abs(xl - xs))
+    assert np.allclose(ql.cpu().numpy(), qs, rtol=1e-4, atol=1e-4)
+    g.close()

@@ -158,7 +158,8 @@ def _u_parity(oracle, w, K, lam=None, seed=1, coupled=True):
 
 
 def test_update_c1(oracle):
-    _u_parity(oracle, get("C1"), 256)
+    _, _, bound = _u_parity(oracle, get("C1"), 256)
+    assert bound <= 5e-6, "coupled U check (A20(ii)) did not run: bound %.3g" % bound
 
 
 def test_update_c3_racecar(oracle):
@@ -166,7 +167,8 @@ def test_update_c3_racecar(oracle):
 
 
 def test_update_c4_quadrotor(oracle):
-    _u_parity(oracle, get("C4"), 4096)
+    _, _, bound = _u_parity(oracle, get("C4"), 4096)
+    assert bound <= 5e-6, "coupled U check (A20(ii)) did not run: bound %.3g" % bound
 
 
 @pytest.mark.parametrize("lam", [None, 30.0])
@@ -596,7 +598,8 @@ def test_sparse_reduction_is_bitwise_dense(cfg, K, lam):
 def test_general_sigma_fast_paths_are_bitwise(cfg):
     """Non-diagonal Sigma (the general one-sample path) at K = 65536: drawing the noise in the
     rollout and (quadrotor) the obstacle grid give the same bits as the separate noise pass and
-    the full search; and the costs stay within tolerance of the oracle."""
+    the full search (GPU against GPU; the oracle parity of correlated Sigma and full R is
+    tests/test_gpu_general_sigma.py)."""
     from paper_1509_01149_b200 import _capi as A
     w = get(cfg)
     m = w.m
