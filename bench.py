@@ -27,36 +27,81 @@ sys.path.insert(0, ROOT)
 METRIC = "MPPI rollout timesteps/sec (K*T per s)"
 UNIT = "K*T/s"
 
-# FP32 FLOPs per sample-step of the rollout kernel (FADD + FMUL + 2 FFMA + 2 FADD2 + 2 FMUL2 +
-# 4 FFMA2 per thread, ncu sass counters / (K*T)); see DESIGN.md "Rollout FLOPs".  None -> not
-# yet measured for that plant (roofline falls back to the kernel's measured share only).
-ROLLOUT_FLOP_PER_SS = {"cartpole": 59.43, "racecar": 249.6,   # profiles/r1_rollout_flops_*_v13.csv
-                       "quadrotor": 464.56}  # profiles/r1_ncu_full_c5_v7.txt (rollout v7, x2)
-# The packed quadrotor rollout with the obstacle candidate grid and the in-kernel noise (the C5
-# path, K_loc >= 65536): FP32 FLOPs, issued thread instructions and DRAM bytes per sample-step,
-# ncu --set full at C5 (profiles/r1_ncu_full_c5_v13.txt).  The kernel also draws the noise
-# (Philox integer work, Box-Muller) so it is issue-bound on a mixed integer/FP32 stream; the
-# FP32-pipe fraction is the roofline, the issue-slot fraction is reported beside it.
-FUSED_QUAD = {"flop": 358.10, "inst": 311.85, "dram_bytes": 15.953}
-# The same kernel with the fused reduction epilogue (MPPI_OPTION_FUSED_REDUCTION, the default):
-# each CTA also forms its samples' weights and weighted noise sums, re-reading the noise it wrote
-# (profiles/r1_ncu_full_c5_v15.txt).  Algorithmic bytes: the noise written and read back once,
-# 2 * 4 m per sample-step (ncu DRAM bytes are below that: part of the re-read hits L2).
-FUSED_QUAD_EPI = {"flop": 366.99, "inst": 320.43, "dram_bytes": 27.84}
+# Roofline numerators per sample-step of each rollout variant (FP32 FLOPs = FADD + FMUL + 2 FFMA +
+# 2 FADD2 + 2 FMUL2 + 4 FFMA2 thread-level SASS counters, thread instructions, DRAM bytes), from
+# the ncu captures of scripts/gpu_roofline_capture.sh, written with the source hash of the tree
+# they measured (profiles/roofline_constants.json, scripts/roofline_constants.py).  bench.py
+# recomputes the hash of the library sources and marks the constants stale when they differ.
+CONSTANTS_PATH = os.path.join(ROOT, "profiles", "roofline_constants.json")
+# the full 50-cylinder search with the noise read from HBM (the v7 packed kernel's ncu count,
+# profiles/r1_ncu_full_c5_v7.txt): the effective-rate comparison only, not executed FLOPs
+FULL_SEARCH_QUAD_FLOP = 464.56
+
+
+def roofline_constants():
+    """{variant key: {flop, inst, dram_bytes, ...}}, and whether they measured this source tree."""
+    try:
+        with open(CONSTANTS_PATH) as f:
+            doc = json.load(f)
+    except Exception:
+        return {}, {"file": None, "stale": True}
+    cur = None
+    try:
+        from paper_1509_01149_b200 import build as B
+        cur = B.source_hash()
+    except Exception:
+        pass
+    meta = {"file": os.path.relpath(CONSTANTS_PATH, ROOT), "source_hash": doc.get("source_hash"),
+            "current_source_hash": cur, "stale": cur is None or cur != doc.get("source_hash"),
+            "git_head": doc.get("git_head")}
+    return doc.get("variants", {}), meta
+
+
+def variant_key(variant, plant):
+    return variant if (variant and ":" in variant) else "%s:%s" % (variant, plant)
+
+
+_B = r"(?:\(bool\))?(true|false|1|0)"
+_I = r"(?:\(int\))?(-?\d+)"
+
+
+def _b(v):
+    return v in ("1", "true")
 
 
 def variant_of(kernels):
-    """The rollout variant the library's dispatch chose, from the mangled device-function names
-    of the last step's launches (mppi_last_kernels): rollout_kernel_x2<NP, GEN, QSTEP, DIAG, EPI>
-    -> "x2[-grid][-fused][-general][-ctg][-epi]", the one-sample kernels -> "scalar"."""
+    """The rollout variant the library's dispatch chose, from the device-function names of the
+    last step's launches (mppi_last_kernels, mangled) or an ncu kernel name (demangled):
+    rollout_kernel_x2<NP, GEN, QSTEP, DIAG, EPI> -> "x2[-grid][-fused][-general][-ctg][-epi]",
+    rollout_kernel<Plant, DIAG, NP, GEN, QSTEP> -> "scalar[-grid][-fused][-general][-ctg]:<plant>"."""
     import re
     for k in kernels:
         mt = re.search(r"rollout_kernel_x2IL(in?)(\d+)ELb([01])ELb([01])ELb([01])ELb([01])E", k)
         if mt:
             np_ = -int(mt.group(2)) if mt.group(1) == "in" else int(mt.group(2))
             gen, qstep, diag, epi = (mt.group(i) == "1" for i in range(3, 7))
+        else:
+            mt = re.search(r"rollout_kernel_x2<\s*%s,\s*%s,\s*%s,\s*%s,\s*%s\s*>" % (_I, _B, _B, _B, _B), k)
+            if mt:
+                np_ = int(mt.group(1))
+                gen, qstep, diag, epi = (_b(mt.group(i)) for i in range(2, 6))
+        if mt:
             return ("x2" + ("-grid" if np_ == -2 else "") + ("-fused" if gen else "") +
                     ("" if diag else "-general") + ("-ctg" if qstep else "") + ("-epi" if epi else ""))
+        mt = re.search(r"rollout_kernelINS_\d+([A-Za-z]+)(?:I.*?E)?ELb([01])EL(in?)(\d+)ELb([01])ELb([01])E", k)
+        if mt:
+            plant = mt.group(1)
+            diag = mt.group(2) == "1"
+            np_ = -int(mt.group(4)) if mt.group(3) == "in" else int(mt.group(4))
+            gen, qstep = mt.group(5) == "1", mt.group(6) == "1"
+        else:
+            mt = re.search(r"rollout_kernel<\s*mppi::([A-Za-z]+)(?:<[^>]*>)?,\s*%s,\s*%s,\s*%s,\s*%s\s*>" % (_B, _I, _B, _B), k)
+            if mt:
+                plant = mt.group(1)
+                diag, np_, gen, qstep = _b(mt.group(2)), int(mt.group(3)), _b(mt.group(4)), _b(mt.group(5))
+        if mt:
+            return ("scalar" + ("-grid" if np_ == -2 else "") + ("-fused" if gen else "") +
+                    ("" if diag else "-general") + ("-ctg" if qstep else "") + ":" + plant.lower())
         if "rollout_kernel" in k:
             return "scalar"
     return None
@@ -257,6 +302,33 @@ def lscpu_model():
     return None
 
 
+def rollout_roofline(variant, plant, K_loc, T, avg_ms, peak, sm_count, sm_max_mhz, consts, meta):
+    """FP32 ALU roofline of one rollout launch: the variant's FLOPs per sample-step (ncu, this
+    source tree unless `stale`) x K_loc T / the launch's CUDA-event time; issue-slot fraction from
+    the instruction count; `traffic` = ncu DRAM bytes of the same capture scaled to this launch."""
+    key = variant_key(variant, plant)
+    c = consts.get(key)
+    units = K_loc * T
+    out = {"kernel": "rollout", "variant": key, "bound": "alu", "unit": "TFLOP/s", "peak": peak,
+           "achieved": None, "frac": None, "traffic": None, "avg_ms": avg_ms,
+           "constants": dict(meta, capture=(c or {}).get("capture"))}
+    if not c or not avg_ms:
+        out["note"] = "no ncu constants for %s" % key
+        return out
+    ach = c["flop"] * units / (avg_ms * 1e-3) / 1e12
+    slots = sm_count * 4 * sm_max_mhz * 1e6
+    out.update({"achieved": ach, "frac": ach / peak, "flop_per_sample_step": c["flop"],
+                "inst_per_sample_step": c["inst"],
+                "issue_frac": c["inst"] / 32.0 * units / (avg_ms * 1e-3) / slots,
+                "traffic": c["dram_bytes"] * units,
+                "algorithmic_bytes_per_launch": None})
+    return out
+
+
+def fp32_peak_now(probe, sm_count, sm_max_mhz):
+    return fp32_peak(probe, sm_count, sm_max_mhz)["peak_tflops"]
+
+
 # ----------------------------------------------------------------------------- reference arm
 def workload_name(cfg, w, K):
     return "%s: %s K=%d T=%d m=%d nu=%g lambda=%g (K/N per GPU)" % (cfg, w.plant, K, w.T, w.m, w.nu, w.lam)
@@ -291,12 +363,13 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------- latency
-def latency(cfg_name, iters=200, warm=20):
+def latency(cfg_name, iters=200, warm=20, K=None):
     import torch
     from mppi_inputs import get
     from paper_1509_01149_b200 import from_workload
     w = get(cfg_name)
-    m = from_workload(w)
+    Kx = K or w.K
+    m = from_workload(w, K=Kx)
     U = torch.tensor(w.U0, device="cuda")
     for i in range(warm):
         m.optimize(w.x0, U, w.seed, i)
@@ -316,10 +389,23 @@ def latency(cfg_name, iters=200, warm=20):
     q = lambda xs, p: sorted(xs)[min(len(xs) - 1, int(round(p * (len(xs) - 1))))]
     launches = m.last_launch_count()
     m.close()
-    return {"K": w.K, "T": w.T, "plant": w.plant, "device_us_p50": q(dev, 0.5),
+    return {"K": Kx, "T": w.T, "plant": w.plant, "device_us_p50": q(dev, 0.5),
             "device_us_p99": q(dev, 0.99), "host_us_p50": q(host, 0.5), "host_us_p99": q(host, 0.99),
             "calls": iters, "kernels_per_call": launches,
-            "KT_per_s_at_p50": w.K * w.T / (q(dev, 0.5) * 1e-6)}
+            "KT_per_s_at_p50": Kx * w.T / (q(dev, 0.5) * 1e-6)}
+
+
+def paper_context_latency():
+    """The paper's operating point beside our latency: K = 1000 rollouts of the
+    cart-pole over a 1 s horizon (T = 50 at 50 Hz, :396), re-optimised every 20 ms (:387) on an
+    unnamed GPU (:10, :343).  Context, not a target: the paper prints no timing."""
+    r = latency("C1", K=1000)
+    r["paper"] = {"K": 1000, "T": 50, "control_period_ms": 20.0, "gpu": "not named",
+                  "implied_KT_per_s_floor": 1000 * 50 / 0.020,
+                  "cite": "PAPER.md:387 (50 Hz), :396 (1 s horizon), :402-403 (K up to 1000)"}
+    r["host_p99_rate_hz"] = 1e6 / r["host_us_p99"]
+    r["device_p99_rate_hz"] = 1e6 / r["device_us_p99"]
+    return r
 
 
 def _safe(fn, *a, **k):
@@ -331,13 +417,16 @@ def _safe(fn, *a, **k):
 
 # ----------------------------------------------------------------------------- other configs
 def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=False,
-               fused_reduction=True, profile=False):
-    """K*T/s of one config on this GPU (graph replay, CUDA events around `steps` steps)."""
+               fused_reduction=True, peak=None, consts=None, meta=None):
+    """K*T/s of one config on this GPU (graph replay, CUDA events around `steps` steps), then a
+    separate profiled pass of the same number of steps (per-kernel CUDA events) for the rollout's
+    FP32 fraction and, where the dense reduction runs as its own kernel, its HBM fraction."""
     import torch
     from mppi_inputs import get
     from paper_1509_01149_b200 import _capi as A, from_workload
     w = get(cfg_name)
-    m = from_workload(w, K=K or w.K)
+    Kx = K or w.K
+    m = from_workload(w, K=Kx)
     if cost_to_go:
         m.set_weighting(True)
     if sparse:      # the sparse skip belongs to the separate K3 reduction
@@ -357,27 +446,38 @@ def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=Fals
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     launched = m.last_kernels()
-    kern = None
-    if profile:     # a separate profiled pass (per-kernel CUDA events), after the timed one
-        m.profile_enable(True)
-        for i in range(steps):
-            m.optimize(w.x0, U, w.seed, warm + steps + i)
-        kt = m.profile_read()
-        m.profile_enable(False)
-        kern = {k: v[0] / v[1] for k, v in kt.items() if v[1]}
-        if not fused_reduction and kern.get("wsum"):
-            b = 4.0 * w.T * (K or w.K) * w.m + 4.0 * (K or w.K)
-            pk = measured_peaks()
-            kern["wsum_hbm_GBps"] = b / (kern["wsum"] * 1e-3) / 1e9
-            kern["wsum_hbm_frac"] = kern["wsum_hbm_GBps"] / pk.get("hbm_gbs", 6650.0)
+    m.profile_enable(True)          # the profiled pass, after the timed one
+    for i in range(steps):
+        m.optimize(w.x0, U, w.seed, warm + steps + i)
+    kt = m.profile_read()
+    m.profile_enable(False)
     m.close()
-    return {"plant": w.plant, "K": K or w.K, "T": w.T, "ms_per_step": ms, "kernel_avg_ms": kern,
-            "KT_per_s": (K or w.K) * w.T / (ms * 1e-3),
-            "weighting": "cost-to-go (PAPER.md:320-322)" if cost_to_go else "trajectory",
-            "rollout": variant_of(launched), "kernels": short_names(launched),
-            "reduction": ("sparse (all-zero weight blocks skipped, bit-identical)" if sparse else
-                          "fused into the rollout" if any("epi_combine" in k for k in launched)
-                          else "dense GEMV")}
+    kern = {k: v[0] / v[1] for k, v in kt.items() if v[1]}
+    out = {"plant": w.plant, "K": Kx, "T": w.T, "ms_per_step": ms, "kernel_avg_ms": kern,
+           "KT_per_s": Kx * w.T / (ms * 1e-3),
+           "weighting": "cost-to-go (PAPER.md:320-322)" if cost_to_go else "trajectory",
+           "rollout": variant_of(launched), "kernels": short_names(launched),
+           "reduction": ("sparse (all-zero weight blocks skipped, bit-identical)" if sparse else
+                         "fused into the rollout" if any("epi_combine" in k for k in launched)
+                         else "dense GEMV")}
+    if peak and kern.get("rollout"):
+        r = rollout_roofline(out["rollout"], w.plant, Kx, w.T, kern["rollout"], peak,
+                             *_sm(), consts or {}, meta or {})
+        out["rollout_fp32"] = {k: r.get(k) for k in ("variant", "achieved", "frac", "issue_frac",
+                                                     "flop_per_sample_step", "avg_ms")}
+        out["rollout_fp32"]["stale_constants"] = (meta or {}).get("stale")
+    if kern.get("wsum") and out["reduction"] == "dense GEMV" and not cost_to_go:
+        b = 4.0 * w.T * Kx * w.m + 4.0 * Kx
+        pk = measured_peaks()
+        out["wsum_hbm_GBps"] = b / (kern["wsum"] * 1e-3) / 1e9
+        out["wsum_hbm_frac"] = out["wsum_hbm_GBps"] / pk.get("hbm_gbs", 6650.0)
+    return out
+
+
+def _sm():
+    import torch
+    props = torch.cuda.get_device_properties(torch.cuda.current_device())
+    return props.multi_processor_count, measured_peaks().get("sm_max_mhz", 1965.0)
 
 
 def c_abi_closed_loop(steps=200):
@@ -528,9 +628,10 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # ---- the timed region: the shipped default path (CUDA-graph replay with programmatic edges
+    # on one GPU; the library's NCCL step at N > 1), no per-kernel events
     clocks = ClockSampler(dev)
     clocks.start()
-    m.profile_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     if world > 1:
@@ -543,11 +644,20 @@ def main():
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    ktimes = m.profile_read()
-    launched = m.last_kernels()     # the kernel sequence of one timed step
-    m.profile_enable(False)
     clk = clocks.stop()
-    launches = sum(v[1] for v in ktimes.values())
+    launched = m.last_kernels()     # the kernel sequence of one timed step
+    per_step_launches = m.last_launch_count() if sh is None else None
+    # ---- the profiled pass: the same number of steps right after, every kernel (and collective)
+    # bracketed by CUDA events on the context stream (direct launches)
+    m.profile_enable(True)
+    for i in range(args.steps):
+        step(args.warmup + args.steps + i, U)
+    ktimes = m.profile_read()
+    m.profile_enable(False)
+    kernel_launches = sum(v[1] for k, v in ktimes.items() if k != "collective")
+    launches = per_step_launches * args.steps if per_step_launches else kernel_launches
+    coll = ktimes.get("collective", (0.0, 0))
+    rank_stats = [float(K // world), ms, coll[0] / max(args.steps, 1), ktimes["rollout"][0] / max(ktimes["rollout"][1], 1)]
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -555,6 +665,12 @@ def main():
         lt = torch.tensor([launches], device="cuda", dtype=torch.int64)
         dist.all_reduce(lt, op=dist.ReduceOp.SUM)
         launches = int(lt.item())
+        rs = torch.tensor(rank_stats, device="cuda", dtype=torch.float64)
+        allrs = [torch.zeros_like(rs) for _ in range(world)]
+        dist.all_gather(allrs, rs)
+        rank_stats = [r.tolist() for r in allrs]
+    else:
+        rank_stats = [rank_stats]
     assert torch.isfinite(U).all(), "U diverged"
     value = K * w.T * args.steps / (ms * 1e-3)
 
@@ -601,50 +717,46 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel (rank 0's launches, CUDA events on its stream)
+    # ---- roofline of the dominant kernel (rank 0's profiled pass, CUDA events on its stream)
     pk = measured_peaks()
     props = torch.cuda.get_device_properties(dev)
     sm_max = (clk or {}).get("sm_max_mhz") or pk.get("sm_max_mhz", 1965.0)
+    consts, cmeta = roofline_constants()
     kern = {k: {"avg_ms": v[0] / v[1] if v[1] else None, "launches": v[1], "share": None}
             for k, v in ktimes.items()}
     tot = sum(v[0] for v in ktimes.values()) or 1.0
     for k, v in ktimes.items():
         kern[k]["share"] = v[0] / tot
-    dom = max(ktimes, key=lambda k: ktimes[k][0])
+    dom = max((k for k in ktimes if k != "collective"), key=lambda k: ktimes[k][0])
     avg_s = kern[dom]["avg_ms"] * 1e-3
     K_loc = K // world
-    roof = {"kernel": dom}
     variant_of_step = variant_of(launched) or rollout_variant(w, K_loc)
+    fp = fp32_peak(probe, props.multi_processor_count, sm_max)
     if dom == "rollout":
-        fp = fp32_peak(probe, props.multi_processor_count, sm_max)
-        variant = variant_of_step
-        fused = variant.startswith("x2-grid-fused")
-        fq = FUSED_QUAD_EPI if variant.endswith("-epi") else FUSED_QUAD
-        fl = fq["flop"] if fused else ROLLOUT_FLOP_PER_SS.get(w.plant)
-        units = K_loc * w.T
-        ach = fl * units / avg_s / 1e12 if fl else None
-        roof.update({"bound": "alu", "achieved": ach, "peak": fp["peak_tflops"], "unit": "TFLOP/s",
-                     "frac": ach / fp["peak_tflops"] if ach else None,
-                     "traffic": fq["dram_bytes"] * units if fused else None,
-                     "algorithmic_bytes_per_launch": ((8.0 if variant.endswith("-epi") else 4.0) * w.m * units
-                                                      + 4.0 * K_loc) if fused else None,
-                     "flop_per_sample_step": fl, "variant": variant, "peak_detail": fp})
-        if fused:   # issue-slot utilisation: 1 warp instruction / cycle / SM sub-partition
-            slots = props.multi_processor_count * 4 * sm_max * 1e6
-            roof["issue_frac"] = fq["inst"] / 32.0 * units / avg_s / slots
-            # the FP32 work of the same step done the direct way (full 50-cylinder search, noise
-            # read from HBM: the v7 kernel's ncu count) over this kernel's time -- an effective
-            # rate, not executed FLOPs
-            eff = ROLLOUT_FLOP_PER_SS["quadrotor"] * units / avg_s / 1e12
-            roof["effective_full_search"] = {"tflops": eff, "frac": eff / fp["peak_tflops"],
-                                             "flop_per_sample_step": ROLLOUT_FLOP_PER_SS["quadrotor"]}
+        roof = rollout_roofline(variant_of_step, w.plant, K_loc, w.T, kern["rollout"]["avg_ms"],
+                                fp["peak_tflops"], props.multi_processor_count, sm_max, consts, cmeta)
+        roof["peak_detail"] = fp
+        roof["peak_source"] = ("max(derived %.1f, FFMA probe, FFMA2 probe) TFLOP/s; derived = SMs x 128 "
+                               "lanes x 2 x max SM clock (B200_PROFILING.md unit counts)" % fp["derived_tflops"])
+        if variant_of_step.startswith("x2-grid-fused"):
+            # algorithmic bytes: eps written once (and, with the fused reduction, read back once)
+            # plus the costs
+            roof["algorithmic_bytes_per_launch"] = ((8.0 if variant_of_step.endswith("-epi") else 4.0)
+                                                    * w.m * K_loc * w.T + 4.0 * K_loc)
+            if w.plant == "quadrotor":
+                eff = FULL_SEARCH_QUAD_FLOP * K_loc * w.T / avg_s / 1e12
+                roof["effective_full_search"] = {"tflops": eff, "frac": eff / fp["peak_tflops"],
+                                                 "flop_per_sample_step": FULL_SEARCH_QUAD_FLOP}
     else:
         algo = 4.0 * w.T * K_loc * w.m + 4.0 * K_loc if dom == "wsum" else 4.0 * w.T * K_loc * w.m
         peak = pk.get("hbm_gbs", 6650.0)
         ach = algo / avg_s / 1e9
-        roof.update({"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "traffic": None, "algorithmic_bytes_per_launch": algo,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"})
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": None, "algorithmic_bytes_per_launch": algo,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"}
+    roof["kernel_timing"] = ("CUDA events around each launch on the context stream, in a profiled "
+                             "pass of the same %d steps right after the timed region (which itself "
+                             "runs the default graph path without events)" % args.steps)
     # secondary rooflines: the HBM-bound reduction and noise kernels
     extra = {}
     if variant_of_step.endswith("-epi"):
@@ -657,6 +769,7 @@ def main():
         b = 4.0 * w.T * K_loc * w.m
         extra["noise_write_GBps"] = b / (kern["noise"]["avg_ms"] * 1e-3) / 1e9
     roof["secondary"] = extra
+    roof["step_share"] = kern[dom]["share"]
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -669,27 +782,39 @@ def main():
     lat = None
     if not args.no_latency and world == 1:
         lat = {c: latency(c) for c in ("C1", "C2")}
+        lat["paper_point_K1000_T50"] = _safe(paper_context_latency)
 
     extra = None
     if not args.no_extra and world == 1:
-        extra = {"configs": {c: throughput(c) for c in ("C3", "C4")},
-                 "C5_sweep": [throughput("C5", K=1 << e, steps=5) for e in (16, 18, 20, 22)],
-                 "C5_cost_to_go": throughput("C5", steps=5, cost_to_go=True),
-                 "C5_sparse_reduction": throughput("C5", steps=5, sparse=True),
-                 "C5_separate_reduction": _safe(throughput, "C5", steps=5, fused_reduction=False,
-                                                profile=True),
+        tp = dict(peak=fp["peak_tflops"], consts=consts, meta=cmeta)
+        extra = {"configs": {c: throughput(c, **tp) for c in ("C1", "C2", "C3", "C4")},
+                 "C5_sweep": [throughput("C5", K=1 << e, steps=5, **tp) for e in (16, 18, 20, 22)],
+                 "C5_cost_to_go": throughput("C5", steps=5, cost_to_go=True, **tp),
+                 "C5_sparse_reduction": throughput("C5", steps=5, sparse=True, **tp),
+                 "C5_separate_reduction": _safe(throughput, "C5", steps=5, fused_reduction=False, **tp),
                  "c_abi_closed_loop": _safe(c_abi_closed_loop),
                  "closed_loop": closed_loop("C2"),
                  "device_closed_loop": device_closed_loop("C2"),
                  "fig1_trend": fig1_trend()}
 
     if extra and args.config == "C5" and not args.K:
-        sep = (extra.get("C5_separate_reduction") or {}).get("kernel_avg_ms") or {}
+        sep = extra.get("C5_separate_reduction") or {}
         if "wsum_hbm_GBps" in sep:   # the dense K x (T m) GEMV as its own kernel (same workload)
-            roof["secondary"]["separate_wsum_ms"] = sep["wsum"]
+            roof["secondary"]["separate_wsum_ms"] = sep["kernel_avg_ms"]["wsum"]
             roof["secondary"]["separate_wsum_hbm_GBps"] = sep["wsum_hbm_GBps"]
             roof["secondary"]["separate_wsum_hbm_frac"] = sep["wsum_hbm_frac"]
     eps_bytes = 4 * w.T * K_loc * w.m
+    multi = None
+    if world > 1:
+        multi = {"ranks": world, "K_loc": K_loc,
+                 "per_rank": [{"rank": i, "K_loc": int(r[0]), "ms_timed_region": r[1],
+                               "collective_ms_per_step": r[2], "rollout_avg_ms": r[3]}
+                              for i, r in enumerate(rank_stats)],
+                 "collectives": ("ncclAllReduce MIN (int64 key, 8 B) + SUM ([eta, A], %d B) on the library "
+                                 "stream (mppi_nccl_attach; communicator from ncclCommInitRank over "
+                                 "torch's NCCL)" % (4 * (1 + w.T * w.m)) if lib_nccl
+                                 else "torch.distributed all_reduce MIN + SUM (split phase)"),
+                 "collective_ms_per_step_max": max(r[2] for r in rank_stats)}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -702,8 +827,10 @@ def main():
                                                           "in-library NCCL MIN + SUM allreduce" if lib_nccl else
                                                           "MIN + SUM allreduce via torch.distributed")},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "gpu_launches_note": ("library kernels per step (mppi_last_launch_count) x steps, summed over ranks"
+                              if per_step_launches else "kernels of the profiled pass (same steps)"),
         "kernel_sequence": short_names(launched),
-        "clocks": clk, "kernels": kern, "latency": lat, "extra": extra,
+        "clocks": clk, "kernels": kern, "latency": lat, "extra": extra, "multi_gpu": multi,
         "device": torch.cuda.get_device_name(dev),
         "backend": args.backend if world > 1 else None,
     }

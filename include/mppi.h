@@ -496,7 +496,9 @@ typedef enum {
                                   suffix-sum and per-step minimum passes) */
     MPPI_KERNEL_FINALIZE = 3,  /* K4 finalize (partials -> [eta, A] -> U) */
     MPPI_KERNEL_SHIFT = 4,     /* K5 shift_kernel */
-    MPPI_KERNEL_KINDS = 5
+    MPPI_KERNEL_COLLECTIVE = 5, /* the NCCL all-reduces of a sharded step (MIN key, SUM [eta, A];
+                                   NCCL's kernels on the context stream, not this library's) */
+    MPPI_KERNEL_KINDS = 6
 } mppi_kernel_kind_t;
 
 typedef struct {

@@ -814,6 +814,53 @@ void oracle_shift(double* U, int32_t T, int32_t m, const double* u_init) {
     for (int i = 0; i < m; ++i) U[(T - 1) * m + i] = u_init[i];
 }
 
+// Crash-decision margin of each sample (conditioning filter, reading A19'): the fp64
+// rollout of sample k; at every step up to and including the first crash (C = 1
+// once the vehicle touches the ground or a cylinder), the distance of the decision from its
+// threshold, min(|z - ground_z|, |surface distance to the nearest cylinder|).  A sample whose
+// margin is below the fp32 trajectory error can legitimately crash one step earlier or later in
+// an fp32 rollout.  Plants other than the quadrotor: +inf.  Returns 0 ok.
+int oracle_crash_margin(const oracle_problem* pb, const double* x0, const double* U,
+                        const float* eps, int64_t K, int32_t nthreads, double* margin) {
+    if (!problem_ok(pb) || K < 0) return 1;
+    double L[16];
+    if (!cholesky(pb->Sigma, pb->m, L)) return 2;
+#ifdef _OPENMP
+    int nt = nthreads > 0 ? nthreads : omp_get_max_threads();
+#pragma omp parallel for num_threads(nt) schedule(static)
+#endif
+    for (int64_t k = 0; k < K; ++k) {
+        double mk = std::numeric_limits<double>::infinity();
+        if (pb->plant == PLANT_QUADROTOR) {
+            const int n = pb->n, m = pb->m;
+            double x[16];
+            for (int i = 0; i < n; ++i) x[i] = x0[i];
+            int crashed = 0;
+            for (int t = 0; t < pb->T && !crashed; ++t) {
+                const float* e = eps + ((int64_t)t * K + k) * m;
+                double F[16], G[16];
+                step_matrices(pb, t, L, F, G);
+                double v[4];
+                for (int i = 0; i < m; ++i) {
+                    double du = 0;
+                    for (int j = 0; j < m; ++j) du += F[i * m + j] * (double)e[j];
+                    v[i] = U[t * m + i] + du;
+                }
+                plant_step<MathD>(pb, x, v, &crashed);
+                double mt = std::fabs(x[2] - pb->params[21]);
+                for (int j = 0; j < pb->n_obstacles; ++j) {
+                    const double dx = x[0] - pb->obstacles[2 * j], dy = x[1] - pb->obstacles[2 * j + 1];
+                    mt = std::min(mt, std::fabs(std::sqrt(dx * dx + dy * dy) - pb->params[22]));
+                }
+                if (!std::isfinite(mt)) mt = 0.0;          // a diverged state: no margin
+                mk = std::min(mk, mt);
+            }
+        }
+        margin[k] = mk;
+    }
+    return 0;
+}
+
 // States of one rollout (for plots/debugging): xs [T+1][n], with the sample's eps column.
 int oracle_trajectory(const oracle_problem* pb, const double* x0, const double* U,
                       const float* eps, int64_t K, int64_t k, double* xs) {

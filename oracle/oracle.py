@@ -99,6 +99,7 @@ def lib():
         L.oracle_shift.argtypes = [dp, C.c_int32, C.c_int32, dp]
         L.oracle_rollout_stepcosts.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int32, dp, C.c_int32]
         L.oracle_update_ctg.argtypes = [pp, dp, fp, C.c_int64, dp, dp, dp]
+        L.oracle_crash_margin.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int32, dp]
         L.oracle_trajectory.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int64, dp]
         _LIB = L
     return _LIB
@@ -325,15 +326,33 @@ def trajectory(pb: Problem, x0, U, eps, k):
     return xs
 
 
-def well_conditioned(pb: Problem, x0, U, eps, ref_costs=None, rel=1e-5, nthreads=0):
+def crash_margin(pb: Problem, x0, U, eps, nthreads=0):
+    """Per-sample distance of the fp64 crash decisions from their thresholds (quadrotor; +inf
+    otherwise), over the steps up to the first crash (reading A19')."""
+    x0 = np.ascontiguousarray(np.asarray(x0, np.float64))
+    U = np.ascontiguousarray(np.asarray(U, np.float64).reshape(pb.T, pb.m))
+    eps = np.ascontiguousarray(np.asarray(eps, np.float32))
+    out = np.zeros(eps.shape[1])
+    assert lib().oracle_crash_margin(pb.ptr(), _dp(x0), _dp(U), _fp(eps), eps.shape[1], nthreads, _dp(out)) == 0
+    return out
+
+
+CRASH_MARGIN = 1e-4     # m; DESIGN.md reading A19' (>= 10x the fp32 position error at 50 m)
+
+
+def well_conditioned(pb: Problem, x0, U, eps, ref_costs=None, rel=1e-5, nthreads=0,
+                     crash_tol=CRASH_MARGIN):
     """sample k is well-conditioned iff both fp32 twins are within
-    rel * max(|S_k|, 1) of the fp64 cost.  Returns (mask, ref_costs)."""
+    rel * max(|S_k|, 1) of the fp64 cost, and (reading A19') no crash decision of its fp64
+    rollout lies within crash_tol of its threshold.  Returns (mask, ref_costs)."""
     if ref_costs is None:
         ref_costs = rollout_costs(pb, x0, U, eps, "fp64", nthreads)
     a = rollout_costs(pb, x0, U, eps, "twin_f32", nthreads)
     b = rollout_costs(pb, x0, U, eps, "twin_f32_via_f64", nthreads)
     scale = np.maximum(np.abs(ref_costs), 1.0)
     mask = (np.abs(a - ref_costs) <= rel * scale) & (np.abs(b - ref_costs) <= rel * scale)
+    if crash_tol:
+        mask &= crash_margin(pb, x0, U, eps, nthreads) >= crash_tol
     return mask, ref_costs
 
 

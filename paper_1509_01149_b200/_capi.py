@@ -96,10 +96,10 @@ class stats_t(C.Structure):
 
 
 class kernel_times_t(C.Structure):
-    _fields_ = [("total_ms", C.c_double * 5), ("launches", C.c_int64 * 5)]
+    _fields_ = [("total_ms", C.c_double * 6), ("launches", C.c_int64 * 6)]
 
 
-KERNEL_NAMES = ["noise", "rollout", "wsum", "finalize", "shift"]
+KERNEL_NAMES = ["noise", "rollout", "wsum", "finalize", "shift", "collective"]
 
 EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize", "mppi_use_graph", "mppi_set_option",
            "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_apply",

@@ -41,6 +41,18 @@ def deps():
         sorted(glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(ROOT, "include", "mppi.h")]
 
 
+def source_hash():
+    """sha256 over the library's sources (kernels, runtime, header): the key that ties a
+    committed ncu capture (profiles/roofline_constants.json) to the code it measured."""
+    import hashlib
+    h = hashlib.sha256()
+    for p in deps():
+        h.update(os.path.relpath(p, ROOT).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def up_to_date():
     if not os.path.exists(LIB):
         return False

@@ -42,7 +42,11 @@ __device__ __forceinline__ void store_eps(float* p, const float* z) {
 // programmatic): a kernel's CTAs may be launched as its predecessor's last CTAs exit; pdl_wait()
 // blocks until the predecessor grid has completed and its memory is visible (a no-op for an
 // ordinary launch).  No kernel triggers its successor early: measured on B200, early triggers
-// let waiting reduction CTAs crowd the rollout (C2 42 -> 118 us).
+// let waiting reduction CTAs crowd the rollout (C2 42 -> 118 us).  Every kernel waits before it
+// reads anything a predecessor writes.  Only the rollout kernels read before the wait, and only
+// inputs no kernel of a step graph writes: U, R, the per-step matrices, obstacles and the cell
+// grid (U is written by finalize, the LAST node of the step graph; the closed-loop graph, where
+// advance writes U before the next step's rollout, uses ordinary edges).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 // Per-thread asynchronous copy of one noise element group (4m bytes) into shared memory
@@ -116,6 +120,7 @@ struct NoiseArgs {
 
 template <int M>
 __global__ void __launch_bounds__(256) noise_kernel(const NoiseArgs a) {
+    pdl_wait();                        // (first node of a step graph today; waits if ever chained)
     const int k = blockIdx.x * 256 + threadIdx.x;
     const int t0 = blockIdx.y * kNoiseTT;
     if (a.key_reset && k == 0 && t0 == 0) *a.key_reset = LLONG_MAX;
@@ -1689,6 +1694,7 @@ struct AdvanceArgs {
 
 template <class Plant>
 __global__ void __launch_bounds__(1024) advance_kernel(const __grid_constant__ AdvanceArgs<typename Plant::Params> a) {
+    pdl_wait();                        // reads U and x written by its predecessors
     constexpr int M = Plant::M;
     extern __shared__ float sUa[];
     const int TM = a.T * M;
@@ -1772,6 +1778,7 @@ struct FkArgs {
 };
 
 __global__ void __launch_bounds__(256) fk_reduce_kernel(const FkArgs a) {
+    pdl_wait();                        // costs and key of the rollout
     const float smin = key_cost(*a.key);
     double s1 = 0.0, s2 = 0.0;
     for (int k = blockIdx.x * 256 + threadIdx.x; k < a.K_loc; k += gridDim.x * 256) {
@@ -1814,6 +1821,7 @@ struct ShiftArgs {
 };
 
 __global__ void __launch_bounds__(1024) shift_kernel(const ShiftArgs a) {
+    pdl_wait();                        // U of the update
     float* U = a.U;
     const int T = a.T, M = a.M;
     const float4 u_init = a.u_init;

@@ -244,6 +244,12 @@ mppi_status_t digest_params(Ctx& c, const mppi_dynamics_t* d, const mppi_cost_t*
             P.w_xy = Q.w_xy; P.w_z = Q.w_z; P.w_yaw = Q.w_yaw; P.w_vel = Q.w_vel;
             P.w_obs = Q.w_obs; P.inv_obs_length = (float)(1.0 / Q.obs_length); P.w_crash = Q.w_crash;
             P.ground_z = Q.ground_z; P.radius = Q.obstacle_radius;
+            {   // the largest float x with sqrtf(x) <= radius (IEEE sqrt is monotone)
+                float x = (float)((double)P.radius * (double)P.radius);
+                while (sqrtf(x) > P.radius) x = nextafterf(x, 0.0f);
+                while (sqrtf(nextafterf(x, INFINITY)) <= P.radius) x = nextafterf(x, INFINITY);
+                P.crash_d2 = x;
+            }
             const int n = Q.n_obstacles;
             c.n_obs_pairs = (n + 1) / 2;
             c.obs_host.assign(c.n_obs_pairs, make_float4(-1e15f, -1e15f, -1e15f, -1e15f));
@@ -721,17 +727,18 @@ static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t s
     mppi_status_t rs = do_rollout(c, x0, U, seed, step, noise, nullptr, &eps);
     c.epi_active = false;
     if (rs) return rs;
-    int r = nccl_min_key(c, &c.d_stats->min_key);
+    int r;
+    { ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_min_key(c, &c.d_stats->min_key); }
     if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(MIN key): %s", nccl_error(r));
     if (c.ctg) {
         // NEXT-1 sharded: local suffix sums and per-t minima -> MIN over the T
         // minima -> per-(t, k) weights and local sums -> SUM of [eta_t (T), A (T m)] -> update
         MPPI_CUDA(launch_ctg(c), "cost-to-go launch");
-        r = nccl_min_f32(c, c.d_ctg_smin, (size_t)c.T);
+        { ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_min_f32(c, c.d_ctg_smin, (size_t)c.T); }
         if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(MIN S_t): %s", nccl_error(r));
         MPPI_CUDA(launch_wsum_ctg(c, eps), "wsum_ctg launch");
         MPPI_CUDA(launch_finalize_ctg(c, nullptr, nullptr, c.d_commbuf), "finalize_ctg (partials) launch");
-        r = nccl_sum_buf(c, c.d_commbuf, (size_t)c.T + (size_t)c.T * c.m);
+        { ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_sum_buf(c, c.d_commbuf, (size_t)c.T + (size_t)c.T * c.m); }
         if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(SUM [eta_t, A]): %s", nccl_error(r));
         MPPI_CUDA(launch_finalize_ctg(c, U, c.d_commbuf, nullptr), "finalize_ctg (apply) launch");
         c.last_eps = eps;
@@ -743,7 +750,7 @@ static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t s
         MPPI_CUDA(launch_wsum(c, eps, &c.d_stats->min_key), "wsum_kernel launch");
     }
     MPPI_CUDA(launch_finalize(c, nullptr, c.d_commbuf, nullptr), "finalize (partials) launch");
-    r = nccl_sum_buf(c, c.d_commbuf, (size_t)1 + (size_t)c.T * c.m);
+    { ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_sum_buf(c, c.d_commbuf, (size_t)1 + (size_t)c.T * c.m); }
     if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(SUM [eta, A]): %s", nccl_error(r));
     MPPI_CUDA(launch_finalize(c, c.d_commbuf, nullptr, U), "finalize (apply) launch");
     c.last_eps = eps;

@@ -17,9 +17,12 @@ def _fptr(t):
     return C.c_void_p(t.data_ptr())
 
 
-def _check_dev(t, shape, dtype, name):
+def _check_dev(t, shape, dtype, name, device=None):
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError("%s must be a CUDA tensor" % name)
+    if device is not None and t.device != device:
+        # a pointer into another GPU's memory would reach the library as a foreign address
+        raise ValueError("%s is on %s but this MPPI context lives on %s" % (name, t.device, device))
     if t.dtype != dtype or not t.is_contiguous() or tuple(t.shape) != tuple(shape):
         raise ValueError("%s must be a contiguous %s tensor of shape %s (got %s %s)"
                          % (name, dtype, tuple(shape), t.dtype, tuple(t.shape)))
@@ -58,6 +61,9 @@ class MPPI:
         self.K_loc, self.k_offset = inf.K_loc, inf.k_offset
         self.device = torch.device("cuda", torch.cuda.current_device())
 
+    def _check_dev(self, t, shape, dtype, name):
+        _check_dev(t, shape, dtype, name, self.device)
+
     # ------------------------------------------------------------------ lifecycle
     def close(self):
         if getattr(self, "ctx", None):
@@ -88,9 +94,9 @@ class MPPI:
     # ------------------------------------------------------------------ the step
     def optimize(self, x0, U, seed=0, step=0, noise=None):
         """mppi_optimize: U (CUDA float32 [T][m]) updated in place."""
-        _check_dev(U, (self.T, self.m), torch.float32, "U")
+        self._check_dev(U, (self.T, self.m), torch.float32, "U")
         if noise is not None:
-            _check_dev(noise, (self.T, self.K_loc, self.m), torch.float32, "noise")
+            self._check_dev(noise, (self.T, self.K_loc, self.m), torch.float32, "noise")
         self._sync_stream()
         x = self._x0(x0)
         A.check(self.lib.mppi_optimize(self.ctx, x.ctypes.data_as(C.POINTER(C.c_float)), _fptr(U),
@@ -117,15 +123,15 @@ class MPPI:
         return U
 
     def rollout_costs(self, x0, U, seed=0, step=0, noise=None, costs=None, min_key=None):
-        _check_dev(U, (self.T, self.m), torch.float32, "U")
+        self._check_dev(U, (self.T, self.m), torch.float32, "U")
         if noise is not None:
-            _check_dev(noise, (self.T, self.K_loc, self.m), torch.float32, "noise")
+            self._check_dev(noise, (self.T, self.K_loc, self.m), torch.float32, "noise")
         if costs is None:
             costs = torch.empty(self.K_loc, dtype=torch.float32, device=U.device)
-        _check_dev(costs, (self.K_loc,), torch.float32, "costs")
+        self._check_dev(costs, (self.K_loc,), torch.float32, "costs")
         if min_key is None:
             min_key = torch.empty(1, dtype=torch.int64, device=U.device)
-        _check_dev(min_key, (1,), torch.int64, "min_key")
+        self._check_dev(min_key, (1,), torch.int64, "min_key")
         self._sync_stream()
         x = self._x0(x0)
         A.check(self.lib.mppi_rollout_costs(
@@ -136,24 +142,24 @@ class MPPI:
     def accumulate(self, global_min_key=None, buf=None):
         if buf is None:
             buf = torch.empty(1 + self.T * self.m, dtype=torch.float32, device=self.device)
-        _check_dev(buf, (1 + self.T * self.m,), torch.float32, "buf")
+        self._check_dev(buf, (1 + self.T * self.m,), torch.float32, "buf")
         if global_min_key is not None:
-            _check_dev(global_min_key, (1,), torch.int64, "global_min_key")
+            self._check_dev(global_min_key, (1,), torch.int64, "global_min_key")
         self._sync_stream()
         A.check(self.lib.mppi_accumulate(
             self.ctx, _fptr(global_min_key) if global_min_key is not None else None, _fptr(buf)))
         return buf
 
     def apply(self, U, buf):
-        _check_dev(U, (self.T, self.m), torch.float32, "U")
-        _check_dev(buf, (1 + self.T * self.m,), torch.float32, "buf")
+        self._check_dev(U, (self.T, self.m), torch.float32, "U")
+        self._check_dev(buf, (1 + self.T * self.m,), torch.float32, "buf")
         self._sync_stream()
         A.check(self.lib.mppi_apply(self.ctx, _fptr(U), _fptr(buf)))
         return U
 
     # ------------------------------------------------------------------ helpers
     def shift(self, U, u_init=None):
-        _check_dev(U, (self.T, self.m), torch.float32, "U")
+        self._check_dev(U, (self.T, self.m), torch.float32, "U")
         ui = _host_f32(np.zeros(self.m) if u_init is None else u_init, self.m, "u_init")
         self._sync_stream()
         A.check(self.lib.mppi_shift(self.ctx, _fptr(U), ui.ctypes.data_as(C.POINTER(C.c_float))))
@@ -162,7 +168,7 @@ class MPPI:
     def noise(self, seed=0, step=0, out=None):
         if out is None:
             out = torch.empty((self.T, self.K_loc, self.m), dtype=torch.float32, device=self.device)
-        _check_dev(out, (self.T, self.K_loc, self.m), torch.float32, "out")
+        self._check_dev(out, (self.T, self.K_loc, self.m), torch.float32, "out")
         self._sync_stream()
         A.check(self.lib.mppi_noise(self.ctx, seed, step, _fptr(out)))
         return out
@@ -201,7 +207,7 @@ class MPPI:
         """mppi_cost_to_go: S~_{t,k} of the last cost-to-go step, CUDA [T][K_loc]."""
         if out is None:
             out = torch.empty((self.T, self.K_loc), dtype=torch.float32, device=self.device)
-        _check_dev(out, (self.T, self.K_loc), torch.float32, "out")
+        self._check_dev(out, (self.T, self.K_loc), torch.float32, "out")
         self._sync_stream()
         A.check(self.lib.mppi_cost_to_go(self.ctx, _fptr(out)))
         return out
@@ -209,8 +215,8 @@ class MPPI:
     def closed_loop(self, x, U, n_steps, seed=0, step0=0, u_init=None, reset_crash=True, log=True):
         """mppi_closed_loop: n_steps of Alg. 1 on the device (x: CUDA [n], U: CUDA [T][m], in/out).
         Returns (x_log [n_steps+1][n], u_log [n_steps][m], q_log [n_steps]) CUDA tensors or None."""
-        _check_dev(x, (self.n,), torch.float32, "x")
-        _check_dev(U, (self.T, self.m), torch.float32, "U")
+        self._check_dev(x, (self.n,), torch.float32, "x")
+        self._check_dev(U, (self.T, self.m), torch.float32, "U")
         ui = _host_f32(np.zeros(self.m) if u_init is None else u_init, self.m, "u_init")
         xl = ul = ql = None
         if log:

@@ -31,7 +31,12 @@ def test_variant_of_packed_names(np_, gen, qstep, diag, epi, want):
 
 def test_variant_of_scalar_and_empty():
     assert bench.variant_of(["_ZN4mppi12noise_kernelILi4EEEvNS_9NoiseArgsE",
-                             "_ZN4mppi14rollout_kernelINS_8CartpoleELb1ELin1ELb0ELb0EEEvNS_11RolloutArgsINS_14CartpoleParamsEEE"]) == "scalar"
+                             "_ZN4mppi14rollout_kernelINS_8CartpoleELb1ELin1ELb0ELb0EEEvNS_11RolloutArgsINS_14CartpoleParamsEEE"]) == "scalar:cartpole"
+    assert bench.variant_of(["_ZN4mppi14rollout_kernelINS_9QuadrotorELb1ELin2ELb1ELb0EEEvNS_11RolloutArgsINT_6ParamsEEE"]) \
+        == "scalar-grid-fused:quadrotor"
+    # ncu's demangled names (the roofline-constant captures) parse to the same variants
+    assert bench.variant_of(["void mppi::rollout_kernel<mppi::Racecar, true, 1, true, false>(x)"]) == "scalar-fused:racecar"
+    assert bench.variant_of(["void mppi::rollout_kernel_x2<(int)-2, 1, 0, 1, 1>(x)"]) == "x2-grid-fused-epi"
     assert bench.variant_of([]) is None
     assert bench.variant_of(["_ZN4mppi15finalize_kernelENS_12FinalizeArgsE"]) is None
 

@@ -225,6 +225,28 @@ def test_quad_crash_freeze(oracle):
     assert c > 0 and np.all(xs[c:] == xs[c])
 
 
+def test_quad_crash_margin_closed_form(oracle):
+    """Reading A19' filter: free fall from z0 with zero thrust (explicit Euler: z_t = z0 -
+    g dt^2 t(t-1)/2) beside a cylinder at horizontal surface distance s: the margin is the
+    smaller of s and the closest approach of z_t to the ground up to the first crash."""
+    T, dt, g = 60, 0.02, 9.81
+    z0, s = 1.0, 0.37
+    pb = P(oracle, "quadrotor", T=T, obstacles=[[0.5 + s, 0.0]])
+    x0 = quad_state(pos=(0, 0, z0), F=(0, 0, 0, 0))
+    U = np.zeros((T, 4))
+    eps = np.zeros((T, 1, 4), np.float32)
+    t = np.arange(1, T + 1)
+    z = z0 - g * dt * dt * t * (t - 1) / 2
+    first = int(np.argmax(z <= 0.0))
+    want = min(s, float(np.min(np.abs(z[:first + 1]))))
+    assert oracle.crash_margin(pb, x0, U, eps)[0] == pytest.approx(want, rel=1e-9)
+    # the ground margin alone (cylinder far away), and +inf for another plant
+    pb = P(oracle, "quadrotor", T=T, obstacles=[[40.0, 0.0]])
+    assert oracle.crash_margin(pb, x0, U, eps)[0] == pytest.approx(float(np.min(np.abs(z[:first + 1]))), rel=1e-9)
+    pc = P(oracle, "cartpole", T=5)
+    assert np.isinf(oracle.crash_margin(pc, [0, 0, 0, 0], np.zeros((5, 1)), np.zeros((5, 1, 1), np.float32))[0])
+
+
 # ----------------------------------------------------------------------------- linear
 def test_linear_plant(oracle):
     A = np.array([[0.0, 1.0], [-2.0, -0.5]])
