@@ -171,6 +171,7 @@ class ClockSampler:
     def __init__(self, gpu_index):
         self.idx = gpu_index
         self.rows = []          # (sm_mhz, sm_max_mhz, {reasons})
+        self.power = []         # W (NVML)
         self.proc = None
         self.thread = None
         self.stop_flag = threading.Event()
@@ -208,6 +209,10 @@ class ClockSampler:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
                 bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                try:
+                    self.power.append(nv.nvmlDeviceGetPowerUsage(self.handle) / 1000.0)
+                except Exception:
+                    pass
                 self.rows.append((float(sm), float(self.sm_max),
                                   {n for n, m in zip(self.REASONS, self.masks) if bits & m}))
             except Exception:
@@ -237,9 +242,13 @@ class ClockSampler:
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = [r[0] for r in self.rows]
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
-                "reasons": sorted(set().union(*[r[2] for r in self.rows])), "samples": len(self.rows),
-                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+               "reasons": sorted(set().union(*[r[2] for r in self.rows])), "samples": len(self.rows),
+               "sm_mhz_min": min(sm), "source": "nvml" if self.nvml is not None else "nvidia-smi"}
+        if self.power:
+            out["power_w_median"] = statistics.median(self.power)
+            out["power_w_max"] = max(self.power)
+        return out
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -453,6 +462,8 @@ def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=Fals
     m.profile_enable(False)
     m.close()
     kern = {k: v[0] / v[1] for k, v in kt.items() if v[1]}
+    tot = sum(v[0] for v in kt.values()) or 1.0
+    share = {k: v[0] / tot for k, v in kt.items() if v[1]}
     out = {"plant": w.plant, "K": Kx, "T": w.T, "ms_per_step": ms, "kernel_avg_ms": kern,
            "KT_per_s": Kx * w.T / (ms * 1e-3),
            "weighting": "cost-to-go (PAPER.md:320-322)" if cost_to_go else "trajectory",
@@ -460,8 +471,10 @@ def throughput(cfg_name, K=None, steps=10, warm=3, cost_to_go=False, sparse=Fals
            "reduction": ("sparse (all-zero weight blocks skipped, bit-identical)" if sparse else
                          "fused into the rollout" if any("epi_combine" in k for k in launched)
                          else "dense GEMV")}
+    out["kernel_share"] = share
     if peak and kern.get("rollout"):
-        r = rollout_roofline(out["rollout"], w.plant, Kx, w.T, kern["rollout"], peak,
+        # the rollout's time in the timed pass: ms/step x its share (as the headline roofline)
+        r = rollout_roofline(out["rollout"], w.plant, Kx, w.T, ms * share["rollout"], peak,
                              *_sm(), consts or {}, meta or {})
         out["rollout_fp32"] = {k: r.get(k) for k in ("variant", "achieved", "frac", "issue_frac",
                                                      "flop_per_sample_step", "avg_ms")}
@@ -649,11 +662,14 @@ def main():
     per_step_launches = m.last_launch_count() if sh is None else None
     # ---- the profiled pass: the same number of steps right after, every kernel (and collective)
     # bracketed by CUDA events on the context stream (direct launches)
+    pclocks = ClockSampler(dev)
+    pclocks.start()
     m.profile_enable(True)
     for i in range(args.steps):
         step(args.warmup + args.steps + i, U)
     ktimes = m.profile_read()
     m.profile_enable(False)
+    pclk = pclocks.stop()
     kernel_launches = sum(v[1] for k, v in ktimes.items() if k != "collective")
     launches = per_step_launches * args.steps if per_step_launches else kernel_launches
     coll = ktimes.get("collective", (0.0, 0))
@@ -728,13 +744,21 @@ def main():
     for k, v in ktimes.items():
         kern[k]["share"] = v[0] / tot
     dom = max((k for k in ktimes if k != "collective"), key=lambda k: ktimes[k][0])
-    avg_s = kern[dom]["avg_ms"] * 1e-3
     K_loc = K // world
     variant_of_step = variant_of(launched) or rollout_variant(w, K_loc)
     fp = fp32_peak(probe, props.multi_processor_count, sm_max)
+    # the rollout's time inside the timed region: the step time x the rollout's share of the
+    # step's kernel time (CUDA events of the profiled pass; a share is insensitive to the clock
+    # drift between the two passes, and step x share also charges the graph's inter-kernel gaps
+    # to the rollout, so it never overstates the rate)
+    dom_ms_timed = ms / args.steps * kern[dom]["share"]
     if dom == "rollout":
-        roof = rollout_roofline(variant_of_step, w.plant, K_loc, w.T, kern["rollout"]["avg_ms"],
+        roof = rollout_roofline(variant_of_step, w.plant, K_loc, w.T, dom_ms_timed,
                                 fp["peak_tflops"], props.multi_processor_count, sm_max, consts, cmeta)
+        pr = rollout_roofline(variant_of_step, w.plant, K_loc, w.T, kern["rollout"]["avg_ms"],
+                              fp["peak_tflops"], props.multi_processor_count, sm_max, consts, cmeta)
+        roof["profiled_pass"] = {"avg_ms": kern["rollout"]["avg_ms"], "achieved": pr["achieved"],
+                                 "frac": pr["frac"], "clocks": pclk}
         roof["peak_detail"] = fp
         roof["peak_source"] = ("max(derived %.1f, FFMA probe, FFMA2 probe) TFLOP/s; derived = SMs x 128 "
                                "lanes x 2 x max SM clock (B200_PROFILING.md unit counts)" % fp["derived_tflops"])
@@ -744,19 +768,22 @@ def main():
             roof["algorithmic_bytes_per_launch"] = ((8.0 if variant_of_step.endswith("-epi") else 4.0)
                                                     * w.m * K_loc * w.T + 4.0 * K_loc)
             if w.plant == "quadrotor":
-                eff = FULL_SEARCH_QUAD_FLOP * K_loc * w.T / avg_s / 1e12
+                eff = FULL_SEARCH_QUAD_FLOP * K_loc * w.T / (dom_ms_timed * 1e-3) / 1e12
                 roof["effective_full_search"] = {"tflops": eff, "frac": eff / fp["peak_tflops"],
                                                  "flop_per_sample_step": FULL_SEARCH_QUAD_FLOP}
     else:
         algo = 4.0 * w.T * K_loc * w.m + 4.0 * K_loc if dom == "wsum" else 4.0 * w.T * K_loc * w.m
         peak = pk.get("hbm_gbs", 6650.0)
-        ach = algo / avg_s / 1e9
+        ach = algo / (dom_ms_timed * 1e-3) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": None, "algorithmic_bytes_per_launch": algo,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"}
-    roof["kernel_timing"] = ("CUDA events around each launch on the context stream, in a profiled "
-                             "pass of the same %d steps right after the timed region (which itself "
-                             "runs the default graph path without events)" % args.steps)
+    roof["avg_ms"] = dom_ms_timed
+    roof["kernel_timing"] = ("avg_ms = timed-region ms/step x the kernel's share of the step's kernel "
+                             "time; the share from CUDA events around each launch on the context "
+                             "stream in a profiled pass of the same %d steps right after the timed "
+                             "region (which itself runs the default graph path without events); "
+                             "profiled_pass gives that pass's own per-launch average" % args.steps)
     # secondary rooflines: the HBM-bound reduction and noise kernels
     extra = {}
     if variant_of_step.endswith("-epi"):
