@@ -141,7 +141,9 @@ typedef struct {
  * (paper: 2.5, 150, 50, 1, 350, 12, 1000).  d = distance from (px, py) to the nearest
  * cylinder surface, max(0, |p - c_j| - obstacle_radius); d = +inf with no
  * obstacles.  C = 1 once pz <= ground_z or d <= 0; C is sticky and freezes the state for the
- * rest of the rollout; the frozen state keeps being charged every step. */
+ * rest of the rollout; the frozen state keeps being charged every step.
+ * w_xy and w_z must be >= 0 (INVALID_ARG otherwise: the rollout folds sqrt(w) into the
+ * position differences). */
 typedef struct {
     float goal[3];
     float w_xy, w_z, w_yaw, w_vel;

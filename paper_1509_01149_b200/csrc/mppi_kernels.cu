@@ -294,7 +294,7 @@ struct ScalarRollout {
         } else {
             slow |= st.deriv_fast(v, a.P, xd);
         }
-        st.update(xd, a.dt);
+        st.update(xd, a.P, a.dt);
         S += q + is;                                                   // S~ += q~
         if constexpr (QSTEP) {                                         // q~_{t-1} = q(x_t) + IS_{t-1}
             if (!first) a.qstep[(size_t)(t - 1) * a.K_loc + k] = q + is_prev;
@@ -397,10 +397,17 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
     // candidate grid (NP == kCellGrid, diagonal path only): centres and cell words
     float2* sCent = reinterpret_cast<float2*>(sMat + (DIAG ? 0 : a.T * 2 * M * M));
     uint32_t* sCells = reinterpret_cast<uint32_t*>(sCent + a.n_cent);
+    // candidate-grid centres in static shared memory (compile-time address: each lane's candidate
+    // load is one LDS with an immediate base, no address arithmetic)
+    __shared__ float sCentXY[NP == kCellGrid ? 2 * kCellMaxCent : 1];
     const int tid = threadIdx.x;
     stage_step_constants<M, DIAG>(a, sObs, sRec, sMat);
     if constexpr (NP == kCellGrid) {
-        for (int i = tid; i < a.n_cent; i += blockDim.x) sCent[i] = a.cent[i];
+        for (int i = tid; i < a.n_cent; i += blockDim.x) {   // SoA: [-x_j], then [-y_j]
+            const float2 c = a.cent[i];
+            sCentXY[i] = c.x;
+            sCentXY[kCellMaxCent + i] = c.y;
+        }
         const int nc = a.cell_nx * a.cell_ny;
         for (int i = tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
     }
@@ -415,7 +422,8 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
         ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
         if constexpr (NP == kCellGrid) {
             ob.cells = sCells;
-            ob.cent = sCent;
+            ob.cx = sCentXY;
+            ob.cy = sCentXY + kCellMaxCent;
             ob.nx = a.cell_nx;
             ob.ny = a.cell_ny;
             ob.ox = a.cell_ox;
@@ -485,6 +493,9 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
     float* sMat = sRing + (GEN ? 0 : 2 * kRolloutThreads * 2 * 4);     // !DIAG: [T][2][M*M]
     float2* sCent = reinterpret_cast<float2*>(sMat + (DIAG ? 0 : a.T * 2 * M * M));
     uint32_t* sCells = reinterpret_cast<uint32_t*>(sCent + a.n_cent);
+    // candidate-grid centres in static shared memory (compile-time address: each lane's candidate
+    // load is one LDS with an immediate base, no address arithmetic)
+    __shared__ float sCentXY[NP == kCellGrid ? 2 * kCellMaxCent : 1];
     const int tid = threadIdx.x;
     // (DIAG keeps its own staging, in this order: the shared helper, or another order, costs
     // the hot loop 4 % through ptxas' register allocation)
@@ -492,7 +503,11 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
         for (int i = tid; i < a.n_obs_pairs; i += blockDim.x) sObs[i] = a.obs[i];
     }
     if constexpr (NP == kCellGrid) {
-        for (int i = tid; i < a.n_cent; i += blockDim.x) sCent[i] = a.cent[i];
+        for (int i = tid; i < a.n_cent; i += blockDim.x) {   // SoA: [-x_j], then [-y_j]
+            const float2 c = a.cent[i];
+            sCentXY[i] = c.x;
+            sCentXY[kCellMaxCent + i] = c.y;
+        }
         const int nc = a.cell_nx * a.cell_ny;
         for (int i = tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
     }
@@ -531,7 +546,8 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
         ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
         if constexpr (NP == kCellGrid) {
             ob.cells = sCells;
-            ob.cent = sCent;
+            ob.cx = sCentXY;
+            ob.cy = sCentXY + kCellMaxCent;
             ob.nx = a.cell_nx;
             ob.ny = a.cell_ny;
             ob.ox = a.cell_ox;
@@ -604,7 +620,7 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
                 amax = fmaxf(amax, st.angle_absmax());
                 st.deriv_fast_unchecked(v, a.P, xd);
             }
-            st.update(xd, a.dt);
+            st.update(xd, a.P, a.dt);
             S = S + (q + is);                                              // S~ += q~
             if constexpr (QSTEP) {
                 if (t > 0) *reinterpret_cast<float2*>(a.qstep + (size_t)(t - 1) * a.K_loc + k) = (q + is_prev).v;
@@ -1712,7 +1728,7 @@ __global__ void __launch_bounds__(1024) advance_kernel(const __grid_constant__ A
         float xd[Plant::N];
         st.template state_cost<-1, true>(true, a.P, ob);
         st.deriv_accurate(u0, a.P, xd);
-        st.update(xd, a.dt);
+        st.update(xd, a.P, a.dt);
         const float q = st.template state_cost<-1, true>(false, a.P, ob);
         float xo[16];
         st.store(xo);
@@ -2277,7 +2293,7 @@ static float host_step_t(const Ctx& c, const typename Plant::Params& P, float* x
     float xd[Plant::N];
     st.template state_cost<-1, true>(true, P, ob);   // cart-pole: sin/cos of the current angle
     st.deriv_accurate(u, P, xd);
-    st.update(xd, c.dt);
+    st.update(xd, P, c.dt);
     const float q = st.template state_cost<-1, true>(false, P, ob);
     float xo[16] = {0};
     st.store(xo);

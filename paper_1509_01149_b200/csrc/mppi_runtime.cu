@@ -244,6 +244,21 @@ mppi_status_t digest_params(Ctx& c, const mppi_dynamics_t* d, const mppi_cost_t*
             P.w_xy = Q.w_xy; P.w_z = Q.w_z; P.w_yaw = Q.w_yaw; P.w_vel = Q.w_vel;
             P.w_obs = Q.w_obs; P.inv_obs_length = (float)(1.0 / Q.obs_length); P.w_crash = Q.w_crash;
             P.ground_z = Q.ground_z; P.radius = Q.obstacle_radius;
+            if (!(Q.w_xy >= 0) || !(Q.w_z >= 0))
+                return fail(MPPI_ERR_INVALID_ARG, "quadrotor: w_xy and w_z must be >= 0");
+            P.gyro_xi = (float)(((double)D.Izz - D.Iyy) / D.Ixx);       // folded constants (plants.cuh)
+            P.gyro_yi = (float)(((double)D.Ixx - D.Izz) / D.Iyy);
+            P.gyro_zi = (float)(((double)D.Iyy - D.Ixx) / D.Izz);
+            P.arm_xi = (float)((double)D.arm / D.Ixx);
+            P.arm_yi = (float)((double)D.arm / D.Iyy);
+            P.yaw_zi = (float)((double)D.yaw_coeff / D.Izz);
+            P.sw_xy = (float)sqrt((double)Q.w_xy);
+            P.sgx = (float)((double)Q.goal[0] * sqrt((double)Q.w_xy));
+            P.sgy = (float)((double)Q.goal[1] * sqrt((double)Q.w_xy));
+            P.sw_z = (float)sqrt((double)Q.w_z);
+            P.sgz = (float)((double)Q.goal[2] * sqrt((double)Q.w_z));
+            P.obs_k2 = (float)(1.4426950408889634 / (double)Q.obs_length);
+            P.obs_rk2 = (float)((double)Q.obstacle_radius * 1.4426950408889634 / (double)Q.obs_length);
             {   // the largest float x with sqrtf(x) <= radius (IEEE sqrt is monotone)
                 float x = (float)((double)P.radius * (double)P.radius);
                 while (sqrtf(x) > P.radius) x = nextafterf(x, 0.0f);
