@@ -325,6 +325,7 @@ void free_ctx(Ctx& c) {
     cudaFree(c.d_flags);
     cudaFree(c.d_epi);
     cudaFree(c.d_eps);
+    cudaFree(c.d_rtab);
     cudaFree(c.d_costs);
     cudaFree(c.d_key_init);
     cudaFree(c.d_part);
@@ -493,8 +494,8 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
 
     cudaError_t e = cudaGetDevice(&c.device);
     if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaGetDevice (no CUDA device?)"); }
-    if (rollout_smem_bytes(c, false) > smem_optin_bytes()) {
-        const size_t need = rollout_smem_bytes(c, false);
+    if (rollout_smem_bytes(c, false) + kRolloutStaticSmem > smem_optin_bytes()) {
+        const size_t need = rollout_smem_bytes(c, false) + kRolloutStaticSmem;
         delete ctx;
         return fail(MPPI_ERR_INVALID_ARG, "T = %d needs %zu B of shared memory per rollout CTA (limit %zu)", T,
                     need, smem_optin_bytes());
@@ -539,6 +540,19 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
         free_ctx(c);
         delete ctx;
         return a;
+    }
+    // BM32 radius table for the packed quadrotor rollout (the C5 path): 32 MB, built once
+    if (plant == MPPI_PLANT_QUADROTOR && m == 4 && K_loc >= kPackedMinK) {
+        if ((a = dalloc(c, &c.d_rtab, (size_t)1 << 23, "BM32 radius table"))) {
+            free_ctx(c);
+            delete ctx;
+            return a;
+        }
+        if ((e = build_radius_table(c)) != cudaSuccess || (e = cudaStreamSynchronize(c.stream)) != cudaSuccess) {
+            free_ctx(c);
+            delete ctx;
+            return cuda_fail(e, "BM32 radius table");
+        }
     }
     e = cudaMallocHost((void**)&c.h_U_pinned, (size_t)T * m * sizeof(float));
     if (e != cudaSuccess) { free_ctx(c); delete ctx; return fail(MPPI_ERR_OOM, "pinned staging"); }
@@ -720,6 +734,7 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
         case MPPI_OPTION_BULK_REDUCTION: ctx->c.tma_wsum = value != 0; return MPPI_OK;
         case MPPI_OPTION_SPARSE_REDUCTION: ctx->c.sparse_wsum = value != 0; return MPPI_OK;
         case MPPI_OPTION_FUSED_REDUCTION: ctx->c.epi = value != 0; return MPPI_OK;
+        case MPPI_OPTION_RADIUS_TABLE: ctx->c.use_rtab = value != 0; return MPPI_OK;
         case MPPI_OPTION_PDL:
             MPPI_CUDA(cudaStreamSynchronize(ctx->c.stream), "stream sync");
             ctx->c.use_pdl = value != 0;
@@ -769,6 +784,15 @@ static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t s
     if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(SUM [eta, A]): %s", nccl_error(r));
     MPPI_CUDA(launch_finalize(c, c.d_commbuf, nullptr, U), "finalize (apply) launch");
     c.last_eps = eps;
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_radius_table(const mppi_ctx* ctx, float* out) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    const Ctx& c = ctx->c;
+    if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
+    if (!c.d_rtab) return fail(MPPI_ERR_UNSUPPORTED, "this context has no BM32 radius table");
+    MPPI_CUDA(cudaMemcpyAsync(out, c.d_rtab, sizeof(float) << 23, cudaMemcpyDeviceToDevice, c.stream), "table copy");
     return MPPI_OK;
 }
 
@@ -893,7 +917,7 @@ mppi_status_t mppi_set_sampling_transform(mppi_ctx* ctx, const double* A) {
     MPPI_CUDA(cudaMemcpy(c.d_mats, mats.data(), mats.size() * sizeof(float), cudaMemcpyHostToDevice), "A_t upload");
     const bool diag_before = c.diag;
     c.diag = false;
-    if (rollout_smem_bytes(c, false) > smem_optin_bytes()) {
+    if (rollout_smem_bytes(c, false) + kRolloutStaticSmem > smem_optin_bytes()) {
         c.diag = diag_before;
         return fail(MPPI_ERR_INVALID_ARG, "per-step transforms at T = %d need %zu B of shared memory per rollout CTA",
                     c.T, rollout_smem_bytes(c, false));
