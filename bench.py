@@ -72,24 +72,21 @@ def _b(v):
 def variant_of(kernels):
     """The rollout variant the library's dispatch chose, from the device-function names of the
     last step's launches (mppi_last_kernels, mangled) or an ncu kernel name (demangled):
-    rollout_kernel_x2<NP, GEN, QSTEP, DIAG, EPI> -> "x2[-grid][-fused[-rtab]][-general][-ctg][-epi]",
+    rollout_kernel_x2<NP, GEN, QSTEP, DIAG, EPI> -> "x2[-grid][-fused][-general][-ctg][-epi]",
     rollout_kernel<Plant, DIAG, NP, GEN, QSTEP> -> "scalar[-grid][-fused][-general][-ctg]:<plant>"."""
     import re
     for k in kernels:
-        mt = re.search(r"rollout_kernel_x2IL(in?)(\d+)EL[bi]([012])ELb([01])ELb([01])ELb([01])E", k)
+        mt = re.search(r"rollout_kernel_x2IL(in?)(\d+)ELb([01])ELb([01])ELb([01])ELb([01])E", k)
         if mt:
             np_ = -int(mt.group(2)) if mt.group(1) == "in" else int(mt.group(2))
-            gen = int(mt.group(3))
-            qstep, diag, epi = (mt.group(i) == "1" for i in range(4, 7))
+            gen, qstep, diag, epi = (mt.group(i) == "1" for i in range(3, 7))
         else:
-            mt = re.search(r"rollout_kernel_x2<\s*%s,\s*%s,\s*%s,\s*%s,\s*%s\s*>" % (_I, _I, _B, _B, _B), k)
+            mt = re.search(r"rollout_kernel_x2<\s*%s,\s*%s,\s*%s,\s*%s,\s*%s\s*>" % (_I, _B, _B, _B, _B), k)
             if mt:
                 np_ = int(mt.group(1))
-                gen = int(mt.group(2))
-                qstep, diag, epi = (_b(mt.group(i)) for i in range(3, 6))
+                gen, qstep, diag, epi = (_b(mt.group(i)) for i in range(2, 6))
         if mt:
-            # GEN: 0 reads eps, 1 draws it, 2 draws it with the BM32 radius table
-            return ("x2" + ("-grid" if np_ == -2 else "") + ("-fused" if gen else "") + ("-rtab" if gen == 2 else "") +
+            return ("x2" + ("-grid" if np_ == -2 else "") + ("-fused" if gen else "") +
                     ("" if diag else "-general") + ("-ctg" if qstep else "") + ("-epi" if epi else ""))
         mt = re.search(r"rollout_kernelINS_\d+([A-Za-z]+)(?:I.*?E)?ELb([01])EL(in?)(\d+)ELb([01])ELb([01])E", k)
         if mt:

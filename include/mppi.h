@@ -302,7 +302,7 @@ typedef enum {
                                           the reduction then reads kilobytes instead of 4 T K m bytes.
                                           Default 0: bench.py measures the dense GEMV the north_star
                                           defines and reports this mode beside it */
-    MPPI_OPTION_FUSED_REDUCTION = 8,   /* packed quadrotor path (K_loc >= 65536, diagonal or general
+    MPPI_OPTION_FUSED_REDUCTION = 8    /* packed quadrotor path (K_loc >= 65536, diagonal or general
                                           Sigma / A_t, obstacle grid, in-kernel noise, trajectory
                                           weights; mppi_last_kernels shows whether it ran): every rollout CTA
                                           weights its samples against its own minimum and forms its
@@ -315,12 +315,6 @@ typedef enum {
                                           bit-identical to the separate pass, and the per-t CTA
                                           minima) and the per-(CTA, t) weighted sums in their
                                           epilogue, rescaled to S_min,t afterwards (default 1) */
-    MPPI_OPTION_RADIUS_TABLE = 9       /* packed quadrotor path with in-kernel noise and the fused
-                                          reduction: the Box-Muller radius r(w) (SURVEY.md Appendix B,
-                                          a function of the 23 bits w >> 9) is read from a 32 MB table
-                                          built at create by the same device function, instead of
-                                          evaluated (log polynomial, IEEE divide and square root);
-                                          bitwise identical noise (default 1) */
 } mppi_option_t;
 
 /* mppi_set_option — execution options that never change results (FUSED_REDUCTION: U to rounding). */
@@ -460,15 +454,7 @@ mppi_status_t mppi_feynman_kac(mppi_ctx* ctx, const float* x0, uint64_t seed, ui
 mppi_status_t mppi_shift(mppi_ctx* ctx, float* U, const float* u_init);
 
 /* mppi_noise — writes this rank's eps [T][K_loc][m] for (seed, step) into `out` (DEVICE). */
-
 mppi_status_t mppi_noise(mppi_ctx* ctx, uint64_t seed, uint64_t step, float* out);
-
-/* mppi_radius_table — copies the context's BM32 radius table (MPPI_OPTION_RADIUS_TABLE):
- * out[n] = r(w) for any w with w >> 9 = n (SURVEY.md Appendix B "Radius"), n < 2^23.
- *   out : DEVICE float [2^23] (32 MB), caller-owned.  Asynchronous on the context stream.
- * UNSUPPORTED when the context has no table (only the packed quadrotor path, K_loc >= 65536, has
- * one); INVALID_ARG for NULL arguments.  A diagnostic for the exhaustive table test. */
-mppi_status_t mppi_radius_table(const mppi_ctx* ctx, float* out);
 
 /* mppi_plant_step — advances the plant one Euler step on the HOST with the same fp32 plant
  * code the rollout kernel runs (environment simulation for closed-loop MPC, Alg. 1 :377).

@@ -22,7 +22,6 @@ MPPI_OPTION_BULK_REDUCTION = 5
 MPPI_OPTION_PDL = 6
 MPPI_OPTION_SPARSE_REDUCTION = 7
 MPPI_OPTION_FUSED_REDUCTION = 8
-MPPI_OPTION_RADIUS_TABLE = 9
 MPPI_WEIGHTS_TRAJECTORY, MPPI_WEIGHTS_COST_TO_GO = 0, 1
 
 
@@ -104,7 +103,7 @@ KERNEL_NAMES = ["noise", "rollout", "wsum", "finalize", "shift", "collective"]
 
 EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize", "mppi_use_graph", "mppi_set_option",
            "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_apply",
-           "mppi_shift", "mppi_noise", "mppi_radius_table", "mppi_feynman_kac", "mppi_closed_loop", "mppi_set_weighting",
+           "mppi_shift", "mppi_noise", "mppi_feynman_kac", "mppi_closed_loop", "mppi_set_weighting",
            "mppi_cost_to_go", "mppi_set_sampling_transform", "mppi_nccl_unique_id", "mppi_nccl_attach",
            "mppi_obstacle_grid", "mppi_plant_step", "mppi_get_stats",
            "mppi_last_launch_count", "mppi_last_kernels", "mppi_profile_enable", "mppi_profile_read", "mppi_last_error", "mppi_status_string", "mppi_abi_version"]
@@ -169,8 +168,6 @@ def lib():
     L.mppi_feynman_kac.restype = st
     L.mppi_noise.argtypes = [vp, C.c_uint64, C.c_uint64, vp]
     L.mppi_noise.restype = st
-    L.mppi_radius_table.argtypes = [vp, vp]
-    L.mppi_radius_table.restype = st
     L.mppi_plant_step.argtypes = [vp, fp, fp, C.POINTER(C.c_int32), fp]
     L.mppi_plant_step.restype = st
     L.mppi_get_stats.argtypes = [vp, C.POINTER(stats_t)]

@@ -97,8 +97,6 @@ struct Ctx {
     bool fuse_noise = true;         // packed rollout draws its own noise (no K1 pass)
     bool tma_wsum = true;           // K3 streams eps with bulk copies (MPPI_OPTION_BULK_REDUCTION)
     bool use_pdl = true;            // programmatic kernel->kernel edges in the step graph (MPPI_OPTION_PDL)
-    bool use_rtab = true;           // packed rollout reads BM32 radii from d_rtab (MPPI_OPTION_RADIUS_TABLE)
-    float* d_rtab = nullptr;        // [2^23] BM32 radius table (quadrotor, K_loc >= kPackedMinK)
     bool sparse_wsum = false;       // K3 skips all-zero-weight column blocks (MPPI_OPTION_SPARSE_REDUCTION)
     bool epi = true;                // packed rollout forms the weighted sums itself (MPPI_OPTION_FUSED_REDUCTION)
     bool epi_active = false;        // set around one optimize step that uses it
@@ -191,7 +189,6 @@ size_t smem_optin_bytes();                             // the device's per-block
 bool grid_on(const Ctx& c);              // the obstacle candidate grid is in use
 bool epi_applies(const Ctx& c);          // the packed rollout can run the fused reduction
 cudaError_t launch_epi_combine(Ctx& c, const long long* key);
-cudaError_t build_radius_table(Ctx& c);     // d_rtab[n] = BM32 r(n << 9), on the context stream
 // NCCL (mppi_nccl.cu): runtime-resolved, 0 on success, >0 ncclResult_t, -1 unavailable
 bool nccl_available();
 int nccl_unique_id(unsigned char* out);

@@ -184,7 +184,6 @@ struct RolloutArgs {
     float lambda;
     // fused noise (GEN kernels): eps[t][k] drawn in-kernel with the K1 counters and written here
     float* eps_out;
-    const float* rtab;      // GEN == 2: the BM32 radius table ([2^23], noise.cuh)
     unsigned step_lo, step_hi;
     PhiloxKeys keys;
 };
@@ -483,7 +482,7 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
 // tile (written moments ago) to form eta_c and A_c[t][j]; the HBM stream of that read overlaps
 // the other CTAs' ALU-bound rollouts instead of running as a separate pass.  epi_combine_kernel
 // rescales by exp(-(m_c - S_min)/lambda) (the online-softmax identity) in a fixed order.
-template <int NP, int GEN, bool QSTEP = false, bool DIAG = true, bool EPI = false>
+template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true, bool EPI = false>
 __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
     rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
     constexpr int M = 4;
@@ -565,7 +564,6 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
         unsigned cur = slot0;
         const unsigned kg = a.k_offset + (unsigned)k;
         float4* op = GEN ? reinterpret_cast<float4*>(a.eps_out + (size_t)k * M) : nullptr;
-        const uint64_t rpol = GEN == 2 ? l2_evict_last_policy() : 0;
         if constexpr (!GEN) {
             cp_async_eps<4>(cur, gp);
             cp_async_eps<4>(cur + 16, gp + 4);
@@ -636,9 +634,8 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
             if constexpr (GEN) {
                 // eps_t enters only the motor-lag derivative and IS_t, late in the step, so it is
                 // drawn in the same iteration and the scheduler overlaps it with the dynamics
-                bm32_normals_x2<4, GEN == 2>(philox4x32_10_dev(kg, (unsigned)t, a.step_lo, a.step_hi, a.keys),
-                                             philox4x32_10_dev(kg + 1u, (unsigned)t, a.step_lo, a.step_hi, a.keys),
-                                             ea, eb, a.rtab, rpol);
+                bm32_normals_x2<4>(philox4x32_10_dev(kg, (unsigned)t, a.step_lo, a.step_hi, a.keys),
+                                   philox4x32_10_dev(kg + 1u, (unsigned)t, a.step_lo, a.step_hi, a.keys), ea, eb);
                 op[0] = make_float4(ea[0], ea[1], ea[2], ea[3]);
                 op[1] = make_float4(eb[0], eb[1], eb[2], eb[3]);
                 op += row / 4;
@@ -1860,18 +1857,6 @@ __global__ void __launch_bounds__(1024) shift_kernel(const ShiftArgs a) {
     }
 }
 
-// BM32 radius table (MPPI_OPTION_RADIUS_TABLE): rtab[n] = r(n << 9) for n < 2^23, by the device
-// function every other noise path evaluates, so a lookup equals the computed radius bit for bit.
-__global__ void __launch_bounds__(256) radius_table_kernel(float* rtab) {
-    const unsigned n = blockIdx.x * 256u + threadIdx.x;
-    if (n < (1u << 23)) rtab[n] = bm32_radius(n << 9);
-}
-
-cudaError_t build_radius_table(Ctx& c) {
-    radius_table_kernel<<<(1u << 23) / 256u, 256, 0, c.stream>>>(c.d_rtab);
-    return cudaGetLastError();
-}
-
 // ============================================================================== launchers
 static cudaEvent_t take_event(Ctx& c) {
     if (!c.ev_pool.empty()) {
@@ -2044,12 +2029,7 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
                 if (c.epi_active && c.gen_eps) {    // fused reduction (EPI)
                     a.epi_part = c.d_epi;
                     a.lambda = c.lambda;
-                    if (c.use_rtab && c.d_rtab) {   // BM32 radii from the table
-                        a.rtab = c.d_rtab;
-                        kern = (const void*)rollout_kernel_x2<NP, 2, false, true, true>;
-                    } else {
-                        kern = (const void*)rollout_kernel_x2<NP, true, false, true, true>;
-                    }
+                    kern = (const void*)rollout_kernel_x2<NP, true, false, true, true>;
                 } else {
                     kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
                 }

@@ -325,7 +325,6 @@ void free_ctx(Ctx& c) {
     cudaFree(c.d_flags);
     cudaFree(c.d_epi);
     cudaFree(c.d_eps);
-    cudaFree(c.d_rtab);
     cudaFree(c.d_costs);
     cudaFree(c.d_key_init);
     cudaFree(c.d_part);
@@ -541,19 +540,6 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
         delete ctx;
         return a;
     }
-    // BM32 radius table for the packed quadrotor rollout (the C5 path): 32 MB, built once
-    if (plant == MPPI_PLANT_QUADROTOR && m == 4 && K_loc >= kPackedMinK) {
-        if ((a = dalloc(c, &c.d_rtab, (size_t)1 << 23, "BM32 radius table"))) {
-            free_ctx(c);
-            delete ctx;
-            return a;
-        }
-        if ((e = build_radius_table(c)) != cudaSuccess || (e = cudaStreamSynchronize(c.stream)) != cudaSuccess) {
-            free_ctx(c);
-            delete ctx;
-            return cuda_fail(e, "BM32 radius table");
-        }
-    }
     e = cudaMallocHost((void**)&c.h_U_pinned, (size_t)T * m * sizeof(float));
     if (e != cudaSuccess) { free_ctx(c); delete ctx; return fail(MPPI_ERR_OOM, "pinned staging"); }
     const long long kinit = LLONG_MAX;
@@ -734,7 +720,6 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
         case MPPI_OPTION_BULK_REDUCTION: ctx->c.tma_wsum = value != 0; return MPPI_OK;
         case MPPI_OPTION_SPARSE_REDUCTION: ctx->c.sparse_wsum = value != 0; return MPPI_OK;
         case MPPI_OPTION_FUSED_REDUCTION: ctx->c.epi = value != 0; return MPPI_OK;
-        case MPPI_OPTION_RADIUS_TABLE: ctx->c.use_rtab = value != 0; return MPPI_OK;
         case MPPI_OPTION_PDL:
             MPPI_CUDA(cudaStreamSynchronize(ctx->c.stream), "stream sync");
             ctx->c.use_pdl = value != 0;
@@ -784,15 +769,6 @@ static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t s
     if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(SUM [eta, A]): %s", nccl_error(r));
     MPPI_CUDA(launch_finalize(c, c.d_commbuf, nullptr, U), "finalize (apply) launch");
     c.last_eps = eps;
-    return MPPI_OK;
-}
-
-mppi_status_t mppi_radius_table(const mppi_ctx* ctx, float* out) {
-    if (mppi_status_t s = check_ctx(ctx)) return s;
-    const Ctx& c = ctx->c;
-    if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
-    if (!c.d_rtab) return fail(MPPI_ERR_UNSUPPORTED, "this context has no BM32 radius table");
-    MPPI_CUDA(cudaMemcpyAsync(out, c.d_rtab, sizeof(float) << 23, cudaMemcpyDeviceToDevice, c.stream), "table copy");
     return MPPI_OK;
 }
 

@@ -239,13 +239,6 @@ class MPPI:
                                           out.ctypes.data_as(C.POINTER(C.c_double))))
         return float(out[0]), float(out[1]), float(out[2])
 
-    def radius_table(self):
-        """mppi_radius_table: the context's BM32 radius table, a CUDA float32 tensor [2^23]."""
-        out = torch.empty(1 << 23, dtype=torch.float32, device=self.device)
-        self._sync_stream()
-        A.check(self.lib.mppi_radius_table(self.ctx, _fptr(out)))
-        return out
-
     def plant_step(self, x, u, crashed=0):
         """mppi_plant_step: host fp32 Euler step; returns (x', q(x'), crashed')."""
         xs = _host_f32(x, self.n, "x").copy()

@@ -13,12 +13,11 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
 # mangled device-function names as cudaFuncGetName returns them
-X2 = "_ZN4mppi17rollout_kernel_x2IL%sELi%dELb%dELb%dELb%dEEEvNS_11RolloutArgsINS_15QuadrotorParamsEEE"
+X2 = "_ZN4mppi17rollout_kernel_x2IL%sELb%dELb%dELb%dELb%dEEEvNS_11RolloutArgsINS_15QuadrotorParamsEEE"
 
 
 @pytest.mark.parametrize("np_,gen,qstep,diag,epi,want", [
     ("in2", 1, 0, 1, 1, "x2-grid-fused-epi"),
-    ("in2", 2, 0, 1, 1, "x2-grid-fused-rtab-epi"),
     ("in2", 1, 0, 1, 0, "x2-grid-fused"),
     ("in2", 1, 0, 0, 1, "x2-grid-fused-general-epi"),
     ("in2", 1, 1, 1, 1, "x2-grid-fused-ctg-epi"),
@@ -38,7 +37,6 @@ def test_variant_of_scalar_and_empty():
     # ncu's demangled names (the roofline-constant captures) parse to the same variants
     assert bench.variant_of(["void mppi::rollout_kernel<mppi::Racecar, true, 1, true, false>(x)"]) == "scalar-fused:racecar"
     assert bench.variant_of(["void mppi::rollout_kernel_x2<(int)-2, 1, 0, 1, 1>(x)"]) == "x2-grid-fused-epi"
-    assert bench.variant_of(["void mppi::rollout_kernel_x2<(int)-2, (int)2, 0, 1, 1>(x)"]) == "x2-grid-fused-rtab-epi"
     assert bench.variant_of([]) is None
     assert bench.variant_of(["_ZN4mppi15finalize_kernelENS_12FinalizeArgsE"]) is None
 
