@@ -620,7 +620,10 @@ def main():
     if lib_nccl:
         ok = 1
         try:
+            t_attach = time.perf_counter()
             m.attach_nccl()
+            print("bench.py: rank %d/%d: mppi_nccl_attach ok (ncclCommInitRank, %.1f ms, K_loc %d)"
+                  % (rank, world, 1e3 * (time.perf_counter() - t_attach), m.K_loc), file=sys.stderr)
         except Exception as e:      # still a GPU path: the split phase + torch.distributed NCCL
             print("bench.py: mppi_nccl_attach failed (%s); using ShardedMPPI" % e, file=sys.stderr)
             ok = 0
@@ -819,6 +822,9 @@ def main():
                  "C5_cost_to_go": throughput("C5", steps=5, cost_to_go=True, **tp),
                  "C5_sparse_reduction": throughput("C5", steps=5, sparse=True, **tp),
                  "C5_separate_reduction": _safe(throughput, "C5", steps=5, fused_reduction=False, **tp),
+                 # the dense K x (T m) GEMV as its own kernel at every sweep K: its HBM fraction
+                 "C5_sweep_separate_reduction": [_safe(throughput, "C5", K=1 << e, steps=5, fused_reduction=False, **tp)
+                                                 for e in (16, 18, 20)],
                  "c_abi_closed_loop": _safe(c_abi_closed_loop),
                  "closed_loop": closed_loop("C2"),
                  "device_closed_loop": device_closed_loop("C2"),
@@ -841,7 +847,9 @@ def main():
                                  "stream (mppi_nccl_attach; communicator from ncclCommInitRank over "
                                  "torch's NCCL)" % (4 * (1 + w.T * w.m)) if lib_nccl
                                  else "torch.distributed all_reduce MIN + SUM (split phase)"),
-                 "collective_ms_per_step_max": max(r[2] for r in rank_stats)}
+                 "collective_ms_per_step_max": max(r[2] for r in rank_stats),
+                 "communicator": ("library-owned NCCL communicator of %d ranks (mppi_nccl_attach; per-rank "
+                                  "init lines on stderr)" % world) if lib_nccl else "torch.distributed process group"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,

@@ -64,6 +64,8 @@ def main(d, out):
                    "issue_active_pct": m.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                    "fma_pipe_pct": m.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
                    "alu_pipe_pct": m.get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "fmaheavy_pipe_pct": m.get("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "fmalite_pipe_pct": m.get("sm__pipe_fmalite_cycles_active.avg.pct_of_peak_sustained_active"),
                    "capture": name, "config": cfg, "K": K, "T": w.T}
             key = v if ":" in v else v + ":" + w.plant
             if key not in res or K > res[key]["K"]:
