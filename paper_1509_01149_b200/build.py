@@ -41,12 +41,19 @@ def deps():
         sorted(glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(ROOT, "include", "mppi.h")]
 
 
+def device_sources():
+    """The files that define the device code (kernels, device functions, their argument structs)."""
+    return [os.path.join(CSRC, f) for f in ("mppi_kernels.cu", "noise.cuh", "plants.cuh", "mppi_internal.h")]
+
+
 def source_hash():
-    """sha256 over the library's sources (kernels, runtime, header): the key that ties a
-    committed ncu capture (profiles/roofline_constants.json) to the code it measured."""
+    """sha256 over the device-code sources: the key that ties a committed ncu capture
+    (profiles/roofline_constants.json: per-sample-step instruction, FLOP and byte counts of the
+    rollout kernels) to the kernels it measured.  Host-only changes (runtime, NCCL glue, the
+    public header) do not change those counts and keep the key."""
     import hashlib
     h = hashlib.sha256()
-    for p in deps():
+    for p in device_sources():
         h.update(os.path.relpath(p, ROOT).encode())
         with open(p, "rb") as f:
             h.update(f.read())

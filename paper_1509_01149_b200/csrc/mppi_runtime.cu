@@ -12,10 +12,17 @@
 #include <string>
 
 #include "mppi_internal.h"
+#include "nvtx3/nvToolsExt.h"   // header-only NVTX v3: named ranges for nsys/ncu (no-ops without a tool)
 
 using namespace mppi;
 
 namespace {
+
+// an NVTX range for the duration of one public call (the host-side enqueue of its work)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 thread_local std::string g_err;
 
@@ -794,6 +801,7 @@ mppi_status_t mppi_nccl_attach(mppi_ctx* ctx, const uint8_t* id) {
 
 mppi_status_t mppi_optimize(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed, uint64_t step,
                             const float* noise) {
+    NvtxRange nvtx_("mppi_optimize");
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
     if (c.nccl) return optimize_nccl(c, x0, U, seed, step, noise);
@@ -913,6 +921,7 @@ mppi_status_t mppi_cost_to_go(mppi_ctx* ctx, float* out) {
 }
 
 mppi_status_t mppi_optimize_host(mppi_ctx* ctx, const float* x0, float* U, uint64_t seed, uint64_t step) {
+    NvtxRange nvtx_("mppi_optimize_host");
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
     if (!U) return fail(MPPI_ERR_INVALID_ARG, "U is NULL");
@@ -928,6 +937,7 @@ mppi_status_t mppi_optimize_host(mppi_ctx* ctx, const float* x0, float* U, uint6
 
 mppi_status_t mppi_rollout_costs(mppi_ctx* ctx, const float* x0, const float* U, uint64_t seed,
                                  uint64_t step, const float* noise, float* costs, int64_t* min_key) {
+    NvtxRange nvtx_("mppi_rollout_costs");
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
     c.last_launches = 0;
@@ -942,6 +952,7 @@ mppi_status_t mppi_rollout_costs(mppi_ctx* ctx, const float* x0, const float* U,
 }
 
 mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, float* buf) {
+    NvtxRange nvtx_("mppi_accumulate");
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
     if (!buf) return fail(MPPI_ERR_INVALID_ARG, "buf is NULL");
@@ -960,6 +971,7 @@ mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, floa
 }
 
 mppi_status_t mppi_apply(mppi_ctx* ctx, float* U, const float* buf) {
+    NvtxRange nvtx_("mppi_apply");
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
     if (!U || !buf) return fail(MPPI_ERR_INVALID_ARG, "U and buf must be non-NULL");
@@ -1059,6 +1071,7 @@ int64_t mppi_last_kernels(const mppi_ctx* ctx, char* buf, int64_t len) {
 mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed, uint64_t step0,
                                int32_t n_steps, const float* u_init, int32_t reset_crash,
                                float* x_log, float* u_log, float* q_log) {
+    NvtxRange nvtx_("mppi_closed_loop");
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
     if (c.world != 1 && !c.nccl)
@@ -1129,6 +1142,7 @@ mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed,
 }
 
 mppi_status_t mppi_feynman_kac(mppi_ctx* ctx, const float* x0, uint64_t seed, uint64_t step, double* out) {
+    NvtxRange nvtx_("mppi_feynman_kac");
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
     if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
