@@ -291,8 +291,9 @@ typedef enum {
                                           (dependent-launch) edges: a kernel's CTAs launch as the
                                           previous kernel's last CTAs exit and wait
                                           (griddepcontrol.wait) for its results; identical results.
-                                          Default 1: on B200 it saves 0.2-1.6 us of p50 latency at
-                                          C1-C3, p99 within run-to-run noise (scripts/ab_latency.py) */
+                                          Default 0: on B200 it saves 1.3-1.5 us of p50 latency at
+                                          C1-C3 but adds 1-5 us at p99 (profiles/r2_ab_latency_pdl.txt,
+                                          scripts/ab_latency.py, 4 x 200 calls per setting) */
     MPPI_OPTION_SPARSE_REDUCTION = 7,  /* with the bulk-copy reduction (K_loc >= 65536, trajectory
                                           weights): a pass over the costs flags the 256-column
                                           blocks holding a nonzero fp32 weight and the

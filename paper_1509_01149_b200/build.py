@@ -41,23 +41,25 @@ def deps():
         sorted(glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(ROOT, "include", "mppi.h")]
 
 
-def device_sources():
-    """The files that define the device code (kernels, device functions, their argument structs)."""
-    return [os.path.join(CSRC, f) for f in ("mppi_kernels.cu", "noise.cuh", "plants.cuh", "mppi_internal.h")]
-
-
-def source_hash():
-    """sha256 over the device-code sources: the key that ties a committed ncu capture
-    (profiles/roofline_constants.json: per-sample-step instruction, FLOP and byte counts of the
-    rollout kernels) to the kernels it measured.  Host-only changes (runtime, NCCL glue, the
-    public header) do not change those counts and keep the key."""
+def source_hash(lib=None):
+    """sha256 of the device code the library carries: the sm_100a cubin compiled from
+    mppi_kernels.cu (every kernel of the step), extracted from libmppi_b200.so with cuobjdump.
+    The key that ties a committed ncu capture (profiles/roofline_constants.json: per-sample-step
+    instruction, FLOP and byte counts of the rollout kernels) to the machine code it measured:
+    host-only changes (runtime, NCCL glue, defaults) leave it unchanged, any kernel change moves it."""
     import hashlib
-    h = hashlib.sha256()
-    for p in device_sources():
-        h.update(os.path.relpath(p, ROOT).encode())
-        with open(p, "rb") as f:
-            h.update(f.read())
-    return h.hexdigest()[:16]
+    import shutil
+    import tempfile
+    lib = lib or LIB
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    with tempfile.TemporaryDirectory() as d:
+        name = "mppi_kernels.sm_100a.cubin"
+        r = subprocess.run([cuobjdump, "-xelf", name, lib], cwd=d, capture_output=True, text=True)
+        path = os.path.join(d, name)
+        if r.returncode != 0 or not os.path.exists(path):
+            raise RuntimeError("cuobjdump -xelf failed: " + r.stderr[-300:])
+        with open(path, "rb") as f:
+            return hashlib.sha256(f.read()).hexdigest()[:16]
 
 
 def up_to_date():

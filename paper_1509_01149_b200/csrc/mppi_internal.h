@@ -96,7 +96,7 @@ struct Ctx {
     bool pack2 = true;              // quadrotor (diagonal): two samples per thread, FP32x2
     bool fuse_noise = true;         // packed rollout draws its own noise (no K1 pass)
     bool tma_wsum = true;           // K3 streams eps with bulk copies (MPPI_OPTION_BULK_REDUCTION)
-    bool use_pdl = true;            // programmatic kernel->kernel edges in the step graph (MPPI_OPTION_PDL)
+    bool use_pdl = false;           // programmatic kernel->kernel edges in the step graph (MPPI_OPTION_PDL, default 0)
     bool sparse_wsum = false;       // K3 skips all-zero-weight column blocks (MPPI_OPTION_SPARSE_REDUCTION)
     bool epi = true;                // packed rollout forms the weighted sums itself (MPPI_OPTION_FUSED_REDUCTION)
     bool epi_active = false;        // set around one optimize step that uses it
