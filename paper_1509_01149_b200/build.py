@@ -41,12 +41,32 @@ def deps():
         sorted(glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(ROOT, "include", "mppi.h")]
 
 
+def _elf_text_sections(blob):
+    """{name: bytes} of the .text.* sections (machine code) of an ELF64 image."""
+    import struct
+    shoff, = struct.unpack_from("<Q", blob, 0x28)
+    shentsize, shnum, shstrndx = struct.unpack_from("<HHH", blob, 0x3A)
+    secs = []
+    for i in range(shnum):
+        name, typ, flags, addr, off, size = struct.unpack_from("<IIQQQQ", blob, shoff + i * shentsize)
+        secs.append((name, off, size))
+    stroff = secs[shstrndx][1]
+    out = {}
+    for name, off, size in secs:
+        end = blob.index(b"\0", stroff + name)
+        nm = blob[stroff + name:end].decode()
+        if nm.startswith(".text."):
+            out[nm] = blob[off:off + size]
+    return out
+
+
 def source_hash(lib=None):
-    """sha256 of the device code the library carries: the sm_100a cubin compiled from
-    mppi_kernels.cu (every kernel of the step), extracted from libmppi_b200.so with cuobjdump.
-    The key that ties a committed ncu capture (profiles/roofline_constants.json: per-sample-step
-    instruction, FLOP and byte counts of the rollout kernels) to the machine code it measured:
-    host-only changes (runtime, NCCL glue, defaults) leave it unchanged, any kernel change moves it."""
+    """sha256 of the machine code the library runs: the .text sections (every kernel's SASS
+    bytes, no line tables or paths) of the sm_100a cubin compiled from mppi_kernels.cu, extracted
+    from libmppi_b200.so with cuobjdump.  The key that ties a committed ncu capture
+    (profiles/roofline_constants.json: per-sample-step instruction, FLOP and byte counts of the
+    rollout kernels) to the code it measured: host-only changes leave it unchanged, any change to
+    a kernel's instructions moves it."""
     import hashlib
     import shutil
     import tempfile
@@ -59,7 +79,12 @@ def source_hash(lib=None):
         if r.returncode != 0 or not os.path.exists(path):
             raise RuntimeError("cuobjdump -xelf failed: " + r.stderr[-300:])
         with open(path, "rb") as f:
-            return hashlib.sha256(f.read()).hexdigest()[:16]
+            blob = f.read()
+    h = hashlib.sha256()
+    for nm, code in sorted(_elf_text_sections(blob).items()):
+        h.update(nm.encode())
+        h.update(code)
+    return h.hexdigest()[:16]
 
 
 def up_to_date():
