@@ -628,7 +628,12 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
             }
         };
         const StepRec* rec = sRec;
-#pragma unroll 2   // two steps per iteration: more scheduling freedom across the step boundary (-1 %)
+#ifndef MPPI_X2_UNROLL
+#define MPPI_X2_UNROLL 2   // two steps per iteration: more scheduling freedom across the step boundary (-1 %)
+#endif
+#define MPPI_PRAGMA_(x) _Pragma(#x)
+#define MPPI_UNROLL_(n) MPPI_PRAGMA_(unroll n)
+        MPPI_UNROLL_(MPPI_X2_UNROLL)
         for (int t = 0; t < a.T; ++t, ++rec) {
             float ea[4], eb[4];
             if constexpr (GEN) {
