@@ -303,7 +303,7 @@ typedef enum {
                                           the reduction then reads kilobytes instead of 4 T K m bytes.
                                           Default 0: bench.py measures the dense GEMV the north_star
                                           defines and reports this mode beside it */
-    MPPI_OPTION_FUSED_REDUCTION = 8    /* packed quadrotor path (K_loc >= 65536, diagonal or general
+    MPPI_OPTION_FUSED_REDUCTION = 8,   /* packed quadrotor path (K_loc >= 65536, diagonal or general
                                           Sigma / A_t, obstacle grid, in-kernel noise, trajectory
                                           weights; mppi_last_kernels shows whether it ran): every rollout CTA
                                           weights its samples against its own minimum and forms its
@@ -316,6 +316,14 @@ typedef enum {
                                           bit-identical to the separate pass, and the per-t CTA
                                           minima) and the per-(CTA, t) weighted sums in their
                                           epilogue, rescaled to S_min,t afterwards (default 1) */
+    MPPI_OPTION_GATHER_COMBINE = 9     /* sharded step with the library's communicator, trajectory
+                                          weights: ONE collective instead of two -- every rank forms
+                                          its weighted sums against its own minimum, an ncclAllGather
+                                          exchanges the [key, eta_r, A_r] records, and every rank
+                                          rescales them by exp(-(S_r - S_min)/lambda) in rank order
+                                          (PAPER.md:320 is invariant to the shift).  k* and S_min
+                                          identical, U equal to rounding (single rank: bitwise)
+                                          (default 1) */
 } mppi_option_t;
 
 /* mppi_set_option — execution options that never change results (FUSED_REDUCTION: U to rounding). */
@@ -371,6 +379,25 @@ mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, floa
  * U DEVICE [T][m] in place.  Per entry: d_i = sum_{j<=i} fl(sL[i][j]*A[t][j]) accumulated in
  * order j = 0..i, U[t][i] = fl(U[t][i] + fl(d_i / eta)). */
 mppi_status_t mppi_apply(mppi_ctx* ctx, float* U, const float* buf);
+
+/* The split phase of the one-collective combine (MPPI_OPTION_GATHER_COMBINE), for callers that
+ * run their own collective (or emulate ranks):
+ *   mppi_gather_record_len — floats per record: 2 (the int64 (cost, k) key) + 1 (eta) + T*m (A)
+ *                            + padding to an even count; -1 for a NULL ctx.
+ *   mppi_accumulate_record — after mppi_rollout_costs: this rank's weights w_k =
+ *                            exp(-(S_k - S_min,r)/lambda) against its OWN minimum S_min,r, its
+ *                            eta_r and A_r, written with its key as one record.
+ *                            record : DEVICE float [mppi_gather_record_len].  Asynchronous.
+ *   mppi_apply_gathered    — n_records records concatenated (DEVICE [n][len], e.g. an all-gather
+ *                            in rank order): S_min = min of the keys, eta = sum_r c_r eta_r,
+ *                            A = sum_r c_r A_r with c_r = exp(-(S_min,r - S_min)/lambda) in record
+ *                            order, then U_t += s L A_t / eta as mppi_apply.
+ *                            Every rank that applies the same records gets the same bits.
+ *                            U : DEVICE [T][m] in/out.  Asynchronous.
+ * INVALID_ARG for NULL pointers or n_records < 1; UNSUPPORTED with cost-to-go weights. */
+int64_t mppi_gather_record_len(const mppi_ctx* ctx);
+mppi_status_t mppi_accumulate_record(mppi_ctx* ctx, float* record);
+mppi_status_t mppi_apply_gathered(mppi_ctx* ctx, float* U, const float* records, int32_t n_records);
 
 /* ---------------------------------------------------------------- general variance transform (NEXT-3) */
 

@@ -22,6 +22,7 @@ MPPI_OPTION_BULK_REDUCTION = 5
 MPPI_OPTION_PDL = 6
 MPPI_OPTION_SPARSE_REDUCTION = 7
 MPPI_OPTION_FUSED_REDUCTION = 8
+MPPI_OPTION_GATHER_COMBINE = 9
 MPPI_WEIGHTS_TRAJECTORY, MPPI_WEIGHTS_COST_TO_GO = 0, 1
 
 
@@ -102,7 +103,7 @@ class kernel_times_t(C.Structure):
 KERNEL_NAMES = ["noise", "rollout", "wsum", "finalize", "shift", "collective"]
 
 EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_optimize", "mppi_use_graph", "mppi_set_option",
-           "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_apply",
+           "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_gather_record_len", "mppi_accumulate_record", "mppi_apply_gathered", "mppi_apply",
            "mppi_shift", "mppi_noise", "mppi_feynman_kac", "mppi_closed_loop", "mppi_set_weighting",
            "mppi_cost_to_go", "mppi_set_sampling_transform", "mppi_nccl_unique_id", "mppi_nccl_attach",
            "mppi_obstacle_grid", "mppi_plant_step", "mppi_get_stats",
@@ -147,6 +148,12 @@ def lib():
     L.mppi_accumulate.restype = st
     L.mppi_apply.argtypes = [vp, vp, vp]
     L.mppi_apply.restype = st
+    L.mppi_gather_record_len.argtypes = [vp]
+    L.mppi_gather_record_len.restype = C.c_int64
+    L.mppi_accumulate_record.argtypes = [vp, vp]
+    L.mppi_accumulate_record.restype = st
+    L.mppi_apply_gathered.argtypes = [vp, vp, vp, C.c_int32]
+    L.mppi_apply_gathered.restype = st
     L.mppi_shift.argtypes = [vp, vp, fp]
     L.mppi_shift.restype = st
     L.mppi_obstacle_grid.argtypes = [C.POINTER(C.c_float), C.c_int32, C.POINTER(C.c_uint32), C.c_int64,

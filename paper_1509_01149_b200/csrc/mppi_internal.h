@@ -160,6 +160,9 @@ struct Ctx {
     // row (e): a communicator the library drives itself (mppi_nccl_attach)
     void* nccl = nullptr;                 // ncclComm_t
     float* d_commbuf = nullptr;           // [T + T*m]: [eta, A] (trajectory: 1 + T*m used) all-reduced across ranks
+    float* d_grec = nullptr;              // one-collective combine: this rank's record [gather_record_len]
+    float* d_gather = nullptr;            // and every rank's, [world][gather_record_len]
+    bool gather_combine = true;           // MPPI_OPTION_GATHER_COMBINE
 };
 
 // Launch (or collect, see Ctx::collect) one kernel whose single parameter is `args`.
@@ -189,6 +192,10 @@ size_t smem_optin_bytes();                             // the device's per-block
 bool grid_on(const Ctx& c);              // the obstacle candidate grid is in use
 bool epi_applies(const Ctx& c);          // the packed rollout can run the fused reduction
 cudaError_t launch_epi_combine(Ctx& c, const long long* key);
+// one-collective combine (MPPI_OPTION_GATHER_COMBINE): record = [key (2 words), eta, A[T*m], pad]
+inline int64_t gather_record_len(const Ctx& c) { return 2 + (((int64_t)c.T * c.m + 1 + 1) & ~(int64_t)1); }
+cudaError_t launch_finalize_record(Ctx& c, float* rec_out);
+cudaError_t launch_finalize_gathered(Ctx& c, const float* gathered, int n_rec, float* U);
 // NCCL (mppi_nccl.cu): runtime-resolved, 0 on success, >0 ncclResult_t, -1 unavailable
 bool nccl_available();
 int nccl_unique_id(unsigned char* out);
@@ -198,6 +205,7 @@ const char* nccl_error(int r);
 int nccl_min_key(Ctx& c, long long* key);
 int nccl_min_f32(Ctx& c, float* buf, size_t count);
 int nccl_sum_buf(Ctx& c, float* buf, size_t count);
+int nccl_all_gather(Ctx& c, const float* send, float* recv, size_t count);   // recv: [world][count]
 int nccl_sum_f64(Ctx& c, double* buf, size_t count);
 cudaError_t launch_fk_reduce(Ctx& c, double* part, int nblk);   // Feynman-Kac partial sums
 cudaError_t launch_ctg(Ctx& c);                                  // cost-to-go + per-t minima

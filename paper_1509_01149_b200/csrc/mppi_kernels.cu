@@ -1247,13 +1247,41 @@ struct FinalizeArgs {
     int T, M;
     float sL[16];
     const float* mats;     // per-t F_t (NEXT-3) or nullptr: U_t += sL A_t / eta
+    // one-collective combine (MPPI_OPTION_GATHER_COMBINE): n_rec records of rec floats each,
+    // [key (int64 as two words), eta_r, A_r[T*M], pad], every rank's sums against its OWN
+    // minimum; rescaled here by exp(-(S_r - S_min)/lambda) in rank order (or nullptr)
+    const float* gathered;
+    int n_rec, rec;
+    float lambda;
+    long long* key_out;    // the global (cost, k) key, or nullptr
+    float* rec_out;        // this rank's record [key, eta, A] (the key from key_src), or nullptr
+    const long long* key_src;
 };
 
 __global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeArgs a) {
     pdl_wait();
     extern __shared__ float sA[];  // [1 + T*M]: eta, A
     const int TM = a.T * a.M;
-    if (a.buf_in) {
+    if (a.gathered) {
+        // global minimum over the records' keys, then the online-softmax rescale of each rank's
+        // sums (the epi_combine arithmetic one level up), accumulated in rank order
+        long long kmin = LLONG_MAX;
+        for (int r = 0; r < a.n_rec; ++r) {
+            const long long kr = *reinterpret_cast<const long long*>(a.gathered + (size_t)r * a.rec);
+            kmin = kr < kmin ? kr : kmin;
+        }
+        const float smin = key_cost(kmin);
+        for (int o = threadIdx.x; o < TM + 1; o += blockDim.x) {
+            float acc = 0.0f;
+            for (int r = 0; r < a.n_rec; ++r) {
+                const float* rr = a.gathered + (size_t)r * a.rec;
+                const float sc = expf(-__fdiv_rn(key_cost(*reinterpret_cast<const long long*>(rr)) - smin, a.lambda));
+                acc = fmaf(sc, rr[2 + o], acc);
+            }
+            sA[o] = acc;
+        }
+        if (a.key_out && threadIdx.x == 0) *a.key_out = kmin;
+    } else if (a.buf_in) {
         for (int o = threadIdx.x; o < TM + 1; o += blockDim.x) sA[o] = a.buf_in[o];
     } else {
         for (int o = threadIdx.x; o < TM; o += blockDim.x) {
@@ -1270,6 +1298,10 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeArgs a) {
     __syncthreads();
     if (a.buf_out)
         for (int o = threadIdx.x; o < TM + 1; o += blockDim.x) a.buf_out[o] = sA[o];
+    if (a.rec_out) {
+        for (int o = threadIdx.x; o < TM + 1; o += blockDim.x) a.rec_out[2 + o] = sA[o];
+        if (threadIdx.x == 0) *reinterpret_cast<long long*>(a.rec_out) = *a.key_src;
+    }
     if (a.stats && threadIdx.x == 0) a.stats->eta = sA[0];
     if (a.U) {
         const float eta = sA[0];
@@ -2243,6 +2275,51 @@ int wsum_blocks_per_sm(int m) {
     if (f && cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsumTmaSmem) == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, kWsumThreads, kWsumTmaSmem);
     return (e == cudaSuccess && n > 0) ? n : 1;
+}
+
+// The one-collective combine's two ends: the local record [local key, eta_r, A_r] (rec_out, sums
+// against this rank's own minimum), and the rescale of n_rec gathered records + the U update.
+cudaError_t launch_finalize_record(Ctx& c, float* rec_out) {
+    FinalizeArgs a{};
+    a.part = c.d_part;
+    a.eta_part = c.d_eta_part;
+    a.n_chunks = c.n_chunks;
+    a.T = c.T;
+    a.M = c.m;
+    a.rec_out = rec_out;
+    a.key_src = &c.d_stats->min_key;
+    const size_t smem = (size_t)(c.T * c.m + 1) * sizeof(float);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int threads = c.T * c.m >= 1024 ? 1024 : ((c.T * c.m + 31) / 32) * 32;
+    return emit(c, (const void*)finalize_kernel, dim3(1), dim3(threads), smem, &a, sizeof(a),
+                MPPI_KERNEL_FINALIZE);
+}
+
+cudaError_t launch_finalize_gathered(Ctx& c, const float* gathered, int n_rec, float* U) {
+    FinalizeArgs a{};
+    a.n_chunks = 0;
+    a.U = U;
+    a.stats = c.d_stats;
+    a.T = c.T;
+    a.M = c.m;
+    for (int i = 0; i < 16; ++i) a.sL[i] = c.sL[i];
+    a.mats = c.per_t ? c.d_mats : nullptr;
+    a.gathered = gathered;
+    a.n_rec = n_rec;
+    a.rec = (int)gather_record_len(c);
+    a.lambda = c.lambda;
+    a.key_out = &c.d_stats->min_key;
+    const size_t smem = (size_t)(c.T * c.m + 1) * sizeof(float);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int threads = c.T * c.m >= 1024 ? 1024 : ((c.T * c.m + 31) / 32) * 32;
+    return emit(c, (const void*)finalize_kernel, dim3(1), dim3(threads), smem, &a, sizeof(a),
+                MPPI_KERNEL_FINALIZE);
 }
 
 cudaError_t launch_finalize(Ctx& c, const float* buf_in, float* buf_out, float* U) {

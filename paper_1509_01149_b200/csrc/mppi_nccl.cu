@@ -1,6 +1,7 @@
 // mppi_nccl.cu — the cross-rank reductions of the K-sharded step (SURVEY §8.5, row e) driven by
 // the library: MIN of the int64 (cost, k) key after the rollouts, SUM of [eta, A] after the local
-// weighted-noise sums, both ncclAllReduce on the context stream between the kernels.
+// weighted-noise sums, both ncclAllReduce on the context stream between the kernels -- or, with
+// the one-collective combine (default), one ncclAllGather of every rank's [key, eta, A] record.
 //
 // NCCL is resolved at run time from the libnccl.so.2 the process already loaded (torch's copy,
 // 2.28) so the library never links a second NCCL; nccl.h is used for the types only.
@@ -19,6 +20,7 @@ struct NcclApi {
     decltype(&ncclGetUniqueId) get_unique_id = nullptr;
     decltype(&ncclCommInitRank) comm_init_rank = nullptr;
     decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclAllGather) all_gather = nullptr;
     decltype(&ncclCommDestroy) comm_destroy = nullptr;
     decltype(&ncclGetErrorString) error_string = nullptr;
     bool ok = false;
@@ -33,9 +35,10 @@ const NcclApi& api() {
         r.get_unique_id = (decltype(r.get_unique_id))dlsym(h, "ncclGetUniqueId");
         r.comm_init_rank = (decltype(r.comm_init_rank))dlsym(h, "ncclCommInitRank");
         r.all_reduce = (decltype(r.all_reduce))dlsym(h, "ncclAllReduce");
+        r.all_gather = (decltype(r.all_gather))dlsym(h, "ncclAllGather");
         r.comm_destroy = (decltype(r.comm_destroy))dlsym(h, "ncclCommDestroy");
         r.error_string = (decltype(r.error_string))dlsym(h, "ncclGetErrorString");
-        r.ok = r.get_unique_id && r.comm_init_rank && r.all_reduce && r.comm_destroy && r.error_string;
+        r.ok = r.get_unique_id && r.comm_init_rank && r.all_reduce && r.all_gather && r.comm_destroy && r.error_string;
         return r;
     }();
     return a;
@@ -87,6 +90,11 @@ int nccl_min_f32(Ctx& c, float* buf, size_t count) {
 // sum of [eta, A[0..T*m)] over ranks, in place
 int nccl_sum_buf(Ctx& c, float* buf, size_t count) {
     return (int)api().all_reduce(buf, buf, count, ncclFloat32, ncclSum, (ncclComm_t)c.nccl, c.stream);
+}
+
+// every rank's record, concatenated in rank order (the one-collective combine)
+int nccl_all_gather(Ctx& c, const float* send, float* recv, size_t count) {
+    return (int)api().all_gather(send, recv, count, ncclFloat32, (ncclComm_t)c.nccl, c.stream);
 }
 
 int nccl_sum_f64(Ctx& c, double* buf, size_t count) {

@@ -322,6 +322,8 @@ void free_ctx(Ctx& c) {
     free_graphs(c);
     nccl_detach(c);
     cudaFree(c.d_commbuf);
+    cudaFree(c.d_grec);
+    cudaFree(c.d_gather);
     for (auto& p : c.ev_pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
     for (auto e : c.ev_pool) cudaEventDestroy(e);
     c.ev_pending.clear();
@@ -727,6 +729,7 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
         case MPPI_OPTION_BULK_REDUCTION: ctx->c.tma_wsum = value != 0; return MPPI_OK;
         case MPPI_OPTION_SPARSE_REDUCTION: ctx->c.sparse_wsum = value != 0; return MPPI_OK;
         case MPPI_OPTION_FUSED_REDUCTION: ctx->c.epi = value != 0; return MPPI_OK;
+        case MPPI_OPTION_GATHER_COMBINE: ctx->c.gather_combine = value != 0; return MPPI_OK;
         case MPPI_OPTION_PDL:
             MPPI_CUDA(cudaStreamSynchronize(ctx->c.stream), "stream sync");
             ctx->c.use_pdl = value != 0;
@@ -750,6 +753,22 @@ static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t s
     c.epi_active = false;
     if (rs) return rs;
     int r;
+    if (!c.ctg && c.gather_combine && c.d_gather) {
+        // one collective: every rank sums its samples against its OWN minimum (the rollout's
+        // key), all-gathers [key, eta_r, A_r], and rescales the records by
+        // exp(-(S_r - S_min)/lambda) in rank order -- identical inputs, identical U on every rank
+        if (epi) {
+            MPPI_CUDA(launch_epi_combine(c, &c.d_stats->min_key), "fused-reduction combine launch");
+        } else {
+            MPPI_CUDA(launch_wsum(c, eps, &c.d_stats->min_key), "wsum_kernel launch");
+        }
+        MPPI_CUDA(launch_finalize_record(c, c.d_grec), "finalize (record) launch");
+        { ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_all_gather(c, c.d_grec, c.d_gather, (size_t)gather_record_len(c)); }
+        if (r) return fail(MPPI_ERR_NCCL, "ncclAllGather(records): %s", nccl_error(r));
+        MPPI_CUDA(launch_finalize_gathered(c, c.d_gather, c.world, U), "finalize (gathered) launch");
+        c.last_eps = eps;
+        return MPPI_OK;
+    }
     { ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_min_key(c, &c.d_stats->min_key); }
     if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(MIN key): %s", nccl_error(r));
     if (c.ctg) {
@@ -793,6 +812,10 @@ mppi_status_t mppi_nccl_attach(mppi_ctx* ctx, const uint8_t* id) {
     if (c.nccl) return fail(MPPI_ERR_INVALID_ARG, "a communicator is already attached");
     if (!c.d_commbuf)
         if (mppi_status_t a = dalloc(c, &c.d_commbuf, (size_t)c.T + (size_t)c.T * c.m, "comm buffer")) return a;
+    if (!c.d_grec)
+        if (mppi_status_t a = dalloc(c, &c.d_grec, (size_t)gather_record_len(c), "gather record")) return a;
+    if (!c.d_gather)
+        if (mppi_status_t a = dalloc(c, &c.d_gather, (size_t)c.world * gather_record_len(c), "gather buffer")) return a;
     const int r = nccl_attach(c, id);
     if (r) return fail(MPPI_ERR_NCCL, "ncclCommInitRank(world %d, rank %d): %s", c.world, c.rank, nccl_error(r));
     free_graphs(c);
@@ -967,6 +990,35 @@ mppi_status_t mppi_accumulate(mppi_ctx* ctx, const int64_t* global_min_key, floa
     if (global_min_key)
         MPPI_CUDA(cudaMemcpyAsync(&c.d_stats->min_key, key, sizeof(long long),
                                   cudaMemcpyDeviceToDevice, c.stream), "global key copy");
+    return MPPI_OK;
+}
+
+int64_t mppi_gather_record_len(const mppi_ctx* ctx) { return ctx ? gather_record_len(ctx->c) : -1; }
+
+mppi_status_t mppi_accumulate_record(mppi_ctx* ctx, float* record) {
+    NvtxRange nvtx_("mppi_accumulate_record");
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (!record) return fail(MPPI_ERR_INVALID_ARG, "record is NULL");
+    if (c.ctg) return fail(MPPI_ERR_UNSUPPORTED, "the split phase uses trajectory weights");
+    if (mppi_status_t s = sticky_check(c)) return s;
+    c.last_launches = 0;
+    c.last_funcs.clear();
+    // the weights against this rank's own minimum (the key mppi_rollout_costs left in the context)
+    MPPI_CUDA(launch_wsum(c, c.last_eps ? c.last_eps : c.d_eps, &c.d_stats->min_key), "wsum_kernel launch");
+    MPPI_CUDA(launch_finalize_record(c, record), "finalize (record) launch");
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_apply_gathered(mppi_ctx* ctx, float* U, const float* records, int32_t n_records) {
+    NvtxRange nvtx_("mppi_apply_gathered");
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    Ctx& c = ctx->c;
+    if (!U || !records || n_records < 1) return fail(MPPI_ERR_INVALID_ARG, "U, records non-NULL and n_records >= 1");
+    if (mppi_status_t s = sticky_check(c)) return s;
+    c.last_launches = 0;
+    c.last_funcs.clear();
+    MPPI_CUDA(launch_finalize_gathered(c, records, n_records, U), "finalize (gathered) launch");
     return MPPI_OK;
 }
 

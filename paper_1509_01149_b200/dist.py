@@ -26,16 +26,31 @@ def shard_range(K, rank, world):
 class ShardedMPPI:
     """Runs one MPPI step of `stepper` (an MPPI context created with rank/world) with the
     cross-rank reductions.  `stepper` needs rollout_costs / accumulate / apply with the
-    semantics of the split-phase C ABI (include/mppi.h)."""
+    semantics of the split-phase C ABI (include/mppi.h); combine="gather" uses the one-collective
+    form instead (accumulate_record / apply_gathered: every rank's [key, eta, A] record against its
+    own minimum, one all-gather, the rescale in rank order -- MPPI_OPTION_GATHER_COMBINE)."""
 
-    def __init__(self, stepper, group=None):
+    def __init__(self, stepper, group=None, combine="allreduce"):
+        if combine not in ("allreduce", "gather"):
+            raise ValueError("combine must be 'allreduce' or 'gather'")
         self.stepper = stepper
         self.group = group
+        self.combine = combine
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
 
     def optimize(self, x0, U, seed=0, step=0, noise=None):
         s = self.stepper
         _, key = s.rollout_costs(x0, U, seed, step, noise)
+        if self.combine == "gather":
+            rec = s.accumulate_record()
+            if self.world > 1:
+                recs = [torch.empty_like(rec) for _ in range(self.world)]
+                dist.all_gather(recs, rec, group=self.group)
+                rec = torch.stack(recs)
+            else:
+                rec = rec.unsqueeze(0)
+            s.apply_gathered(U, rec)
+            return U
         if self.world > 1:
             dist.all_reduce(key, op=dist.ReduceOp.MIN, group=self.group)
         buf = s.accumulate(key)

@@ -150,6 +150,29 @@ class MPPI:
             self.ctx, _fptr(global_min_key) if global_min_key is not None else None, _fptr(buf)))
         return buf
 
+    def gather_record_len(self):
+        return int(self.lib.mppi_gather_record_len(self.ctx))
+
+    def accumulate_record(self, out=None):
+        """mppi_accumulate_record: this rank's [key, eta, A] record against its own minimum (CUDA fp32)."""
+        n = self.gather_record_len()
+        if out is None:
+            out = torch.empty(n, dtype=torch.float32, device=self.device)
+        self._check_dev(out, (n,), torch.float32, "record")
+        self._sync_stream()
+        A.check(self.lib.mppi_accumulate_record(self.ctx, _fptr(out)))
+        return out
+
+    def apply_gathered(self, U, records):
+        """mppi_apply_gathered: records [n][len] (CUDA fp32, e.g. an all-gather in rank order)."""
+        self._check_dev(U, (self.T, self.m), torch.float32, "U")
+        n = records.shape[0] if records.dim() == 2 else 1
+        self._check_dev(records, (n, self.gather_record_len()) if records.dim() == 2 else (self.gather_record_len(),),
+                        torch.float32, "records")
+        self._sync_stream()
+        A.check(self.lib.mppi_apply_gathered(self.ctx, _fptr(U), _fptr(records), n))
+        return U
+
     def apply(self, U, buf):
         self._check_dev(U, (self.T, self.m), torch.float32, "U")
         self._check_dev(buf, (1 + self.T * self.m,), torch.float32, "buf")

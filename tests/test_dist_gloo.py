@@ -56,6 +56,24 @@ class OracleShard:
         U += torch.tensor((A @ self.L.T) / b[0], dtype=U.dtype)
         return U
 
+    # the one-collective form (MPPI_OPTION_GATHER_COMBINE): [S_min,r, k*_r, eta_r, A_r] against
+    # this shard's own minimum; the combine rescales by exp(-(S_min,r - S_min)/lambda)
+    def accumulate_record(self):
+        k = int(np.argmin(self.costs))
+        smin = float(self.costs[k])
+        w = np.exp(-(self.costs.astype(np.float64) - smin) / self.pb.lam)
+        A = np.einsum("k,tkj->tj", w, self.eps.astype(np.float64))
+        return torch.tensor(np.concatenate([[smin, self.k0 + k, w.sum()], A.ravel()]), dtype=torch.float64)
+
+    def apply_gathered(self, U, recs):
+        r = recs.numpy()
+        smin = r[:, 0].min()
+        c = np.exp(-(r[:, 0] - smin) / self.pb.lam)
+        eta = np.sum(c * r[:, 2])
+        A = (c[:, None] * r[:, 3:]).sum(axis=0).reshape(self.pb.T, self.pb.m)
+        U += torch.tensor((A @ self.L.T) / eta, dtype=U.dtype)
+        return U
+
 
 def _free_port():
     s = socket.socket()
@@ -65,7 +83,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cfg, K, q):
+def _worker(rank, world, port, cfg, K, q, combine="allreduce"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -74,7 +92,7 @@ def _worker(rank, world, port, cfg, K, q):
     w = get(cfg)
     pb = O.Problem(w.plant, T=w.T, dt=w.dt, lam=w.lam, nu=w.nu, Sigma=w.Sigma, R=w.R,
                    obstacles=w.obstacles if w.plant == "quadrotor" else None)
-    sh = ShardedMPPI(OracleShard(O, pb, K, rank, world))
+    sh = ShardedMPPI(OracleShard(O, pb, K, rank, world), combine=combine)
     assert sh.world == world
     U = torch.tensor(w.U0.astype(np.float64))
     for step in range(2):
@@ -83,13 +101,16 @@ def _worker(rank, world, port, cfg, K, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cfg,K", [("C1", 256), ("C3", 512)])
-def test_sharded_step_world2_matches_single(oracle, cfg, K):
+@pytest.mark.parametrize("cfg,K,combine", [("C1", 256, "allreduce"), ("C3", 512, "allreduce"),
+                                           ("C1", 256, "gather"), ("C3", 512, "gather")])
+def test_sharded_step_world2_matches_single(oracle, cfg, K, combine):
+    """Both combines (MIN + SUM all-reduce; one all-gather of per-rank records rescaled to the
+    global minimum) give the single-process step (PAPER.md:320 is invariant to the shift)."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, K, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, K, q, combine)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in range(world))
