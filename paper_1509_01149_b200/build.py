@@ -61,8 +61,8 @@ def _elf_text_sections(blob):
 
 
 def source_hash(lib=None):
-    """sha256 of the machine code the library runs: the .text sections (every kernel's SASS
-    bytes, no line tables or paths) of the sm_100a cubin compiled from mppi_kernels.cu, extracted
+    """sha256 of the rollout kernels' machine code: the .text sections (SASS bytes, no line tables
+    or paths) of every rollout_kernel* in the sm_100a cubin compiled from mppi_kernels.cu, extracted
     from libmppi_b200.so with cuobjdump.  The key that ties a committed ncu capture
     (profiles/roofline_constants.json: per-sample-step instruction, FLOP and byte counts of the
     rollout kernels) to the code it measured: host-only changes leave it unchanged, any change to
@@ -82,8 +82,9 @@ def source_hash(lib=None):
             blob = f.read()
     h = hashlib.sha256()
     for nm, code in sorted(_elf_text_sections(blob).items()):
-        h.update(nm.encode())
-        h.update(code)
+        if "rollout_kernel" in nm:          # the kernels the constants describe
+            h.update(nm.encode())
+            h.update(code)
     return h.hexdigest()[:16]
 
 
