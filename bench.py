@@ -843,10 +843,10 @@ def main():
                  "per_rank": [{"rank": i, "K_loc": int(r[0]), "ms_timed_region": r[1],
                                "collective_ms_per_step": r[2], "rollout_avg_ms": r[3]}
                               for i, r in enumerate(rank_stats)],
-                 "collectives": ("ncclAllReduce MIN (int64 key, 8 B) + SUM ([eta, A], %d B) on the library "
-                                 "stream (mppi_nccl_attach; communicator from ncclCommInitRank over "
-                                 "torch's NCCL)" % (4 * (1 + w.T * w.m)) if lib_nccl
-                                 else "torch.distributed all_reduce MIN + SUM (split phase)"),
+                 "collectives": ("ncclAllGather of every rank's [key, eta, A] record (%d B per rank) on the "
+                                 "library stream, rescaled in rank order (MPPI_OPTION_GATHER_COMBINE; "
+                                 "mppi_nccl_attach, ncclCommInitRank over torch's NCCL)" % (4 * (2 + ((w.T * w.m + 2) & ~1)))
+                                 if lib_nccl else "torch.distributed all_reduce MIN + SUM (split phase)"),
                  "collective_ms_per_step_max": max(r[2] for r in rank_stats),
                  "communicator": ("library-owned NCCL communicator of %d ranks (mppi_nccl_attach; per-rank "
                                   "init lines on stderr)" % world) if lib_nccl else "torch.distributed process group"}
@@ -859,7 +859,8 @@ def main():
                    "K": K, "K_per_gpu": K_loc, "T": w.T, "n_obstacles": int(len(w.obstacles)),
                    "l2": "inputs larger than L2 (noise %.1f GB per GPU per step)" % (eps_bytes / 1e9),
                    "parallelism": "K-sharded dp%d, %s" % (world, "single GPU" if world == 1 else
-                                                          "in-library NCCL MIN + SUM allreduce" if lib_nccl else
+                                                          "in-library NCCL: one all-gather of per-rank [key, eta, A] records"
+                                                          if lib_nccl else
                                                           "MIN + SUM allreduce via torch.distributed")},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "gpu_launches_note": ("library kernels per step (mppi_last_launch_count) x steps, summed over ranks"
