@@ -294,10 +294,19 @@ def cpu_baseline(w, steps=1, k_sample=None):
         r = O.optimize(pb, w.x0, U, eps, nthreads=cores)
         U = r["U"]
     dt = time.perf_counter() - t0
+    # one core (SURVEY §8.4 asks for the single-threaded oracle beside the OpenMP one): the
+    # rollouts of a quarter of the sample on one thread
+    K1 = max(4, K // 4)
+    eps = O.noise(w.seed, 0, w.T, K1, w.m)
+    t1 = time.perf_counter()
+    O.rollout_costs(pb, w.x0, w.U0.astype(np.float64), eps, nthreads=1)
+    d1 = time.perf_counter() - t1
     return {"value": K * w.T * steps / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": "%d step(s) of %s at K=%d (of %d), T=%d: noise + rollouts (OpenMP over k) "
                       "+ k-ordered reduction, fp64" % (steps, w.name, K, w.K, w.T),
-            "seconds": dt}
+            "seconds": dt,
+            "one_core_rollouts_KT_per_s": K1 * w.T / d1,
+            "one_core_sample": "rollouts only (fp64, 1 thread) at K=%d, T=%d" % (K1, w.T)}
 
 
 def lscpu_model():
