@@ -151,6 +151,9 @@ def test_null_arguments(capi):
     assert L.mppi_info(None, None) == 1
     L.mppi_destroy(None)
     assert L.mppi_last_launch_count(None) == 0
+    assert L.mppi_gather_record_len(None) == -1
+    assert L.mppi_accumulate_record(None, None) == 1
+    assert L.mppi_apply_gathered(None, None, None, 1) == 1
     assert capi.lib().mppi_status_string(2) == b"MPPI_ERR_NOT_SPD"
 
 
