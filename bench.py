@@ -340,6 +340,15 @@ def rollout_roofline(variant, plant, K_loc, T, avg_ms, peak, sm_count, sm_max_mh
                 "issue_frac": c["inst"] / 32.0 * units / (avg_ms * 1e-3) / slots,
                 "traffic": c["dram_bytes"] * units,
                 "algorithmic_bytes_per_launch": None})
+    heavy = c.get("fmaheavy_pipe_pct")
+    if heavy:
+        # the binding pipe: every packed FP32 op and every IMAD (Philox) occupies
+        # the FMA-heavy pipe; the same instruction stream with that pipe 100 % busy would execute
+        # frac / (heavy / 100) of the FP32 peak -- the ceiling of this instruction mix
+        out["pipes_ncu_pct"] = {"fmaheavy": heavy, "fmalite": c.get("fmalite_pipe_pct"),
+                                "alu": c.get("alu_pipe_pct"), "issue": c.get("issue_active_pct"),
+                                "capture": c.get("capture")}
+        out["frac_ceiling_of_mix"] = out["frac"] / (heavy / 100.0)
     return out
 
 
