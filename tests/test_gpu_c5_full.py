@@ -55,7 +55,7 @@ def test_every_sample_at_k65536_full_horizon(oracle):
     ok, ref = oracle.well_conditioned(problem(oracle, w), w.x0, w.U0, eps)
     err = np.abs(c - ref) / np.maximum(np.abs(ref), 1.0)
     excluded = 1.0 - ok.mean()
-    print("K=65536 T=200: excluded %.5f, max err on kept %.3g, max err overall %.3g"
+    print("PARITY C5 kernel K=65536 T=200 every sample: excluded %.5f, max rel err on kept %.3g, overall %.3g"
           % (excluded, err[ok].max(), err.max()))
     bad = np.nonzero(ok & (err > COST_RTOL))[0]
     assert bad.size == 0, "well-conditioned samples over 1e-4: %s" % bad[:10]
@@ -86,7 +86,8 @@ def test_4096_random_columns_of_c5(oracle):
     ok, ref = oracle.well_conditioned(problem(oracle, w), w.x0, w.U0, ref_eps)
     c = costs.cpu().numpy()[ks].astype(np.float64)
     err = np.abs(c - ref) / np.maximum(np.abs(ref), 1.0)
-    print("C5 4096 columns: excluded %.5f, max err on kept %.3g" % (1 - ok.mean(), err[ok].max()))
+    print("PARITY C5 K=2^22 4096 columns: noise bitwise, excluded %.5f, max rel err on kept %.3g"
+          % (1 - ok.mean(), err[ok].max()))
     assert np.all(err[ok] <= COST_RTOL)
     assert ok.mean() >= 0.99
 

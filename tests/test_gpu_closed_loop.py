@@ -127,7 +127,7 @@ def test_device_loop_step_by_step_against_oracle(oracle, cfg, K):
     ui = np.zeros(w.m, np.float32)
     x = torch.tensor(w.x0, device="cuda")
     U = torch.tensor(w.U0, device="cuda")
-    steps, crashed, coupled = 10, 0, 0
+    steps, crashed, coupled, worst = 10, 0, 0, 0.0
     xs, us = [w.x0.copy()], []
     for i in range(steps):
         x_i = x.cpu().numpy().copy()
@@ -157,9 +157,12 @@ def test_device_loop_step_by_step_against_oracle(oracle, cfg, K):
         assert abs(ql - q_ref) <= 1e-5 * max(abs(q_ref), 1.0)
         # shift
         assert np.array_equal(U_now, oracle.shift(U_after.astype(np.float32), ui).astype(np.float32))
+        worst = max(worst, float(np.max(np.abs(xl[1] - x_ref) / scale)))
         xs.append(xl[1].copy())
         us.append(ul[0].copy())
     assert coupled >= steps // 2, "coupled U check ran on %d of %d steps" % (coupled, steps)
+    print("PARITY closed loop %s K=%d: 10 steps vs oracle, coupled U on %d steps, max plant-step rel err %.3g"
+          % (cfg, K, coupled, worst))
     # the 10-step graph loop equals the step-by-step loop
     x = torch.tensor(w.x0, device="cuda")
     U = torch.tensor(w.U0, device="cuda")

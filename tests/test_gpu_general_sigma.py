@@ -87,6 +87,9 @@ def run(oracle, w, K, lam, seed=3, step=0):
     coupled = bound <= 5e-6
     if coupled:
         assert np.max(np.abs(U_gpu - full["U"])) <= U_ATOL
+    print("PARITY general Sigma/R %s K=%d lambda=%g: max rel err %.3g (excluded %.4f), decoupled |dU| %.3g, "
+          "coupled %s" % (w.name, K, lam, err[ok].max(), 1 - ok.mean(), np.max(np.abs(U_gpu - Ud)),
+                          "%.3g" % np.max(np.abs(U_gpu - full["U"])) if coupled else "not asserted"))
     return dict(kernels=kernels, excluded=1 - ok.mean(), coupled=coupled, err=err[ok].max())
 
 

@@ -77,6 +77,8 @@ def _costs_parity(oracle, w, K, T=None, max_excluded=None, seed=None):
     assert bad.size == 0, "well-conditioned samples over 1e-4: %s (max err %.3g)" % (bad[:10], err[ok].max())
     if max_excluded is not None:
         assert excluded <= max_excluded, "excluded fraction %.4f" % excluded
+    print("PARITY costs %s K=%d T=%d: max rel err on well-conditioned %.3g (bar 1e-4), excluded %.4f"
+          % (w.name, K, T, err[ok].max(), excluded))
     return costs, ref, key, m, excluded, err
 
 
@@ -154,6 +156,9 @@ def _u_parity(oracle, w, K, lam=None, seed=1, coupled=True):
     bound = np.sum(wbar * np.abs(dS) * dev) / lam
     if coupled and bound <= 5e-6:
         assert np.max(np.abs(U_gpu - ref["U"])) <= U_ATOL
+    print("PARITY U %s K=%d lambda=%g: decoupled max |dU| %.3g, coupled %s (bound %.3g) (bar 1e-5)"
+          % (w.name, K, lam, np.max(np.abs(U_gpu - Ud)),
+             "%.3g" % np.max(np.abs(U_gpu - ref["U"])) if bound <= 5e-6 else "not asserted", bound))
     return U_gpu, ref, bound
 
 
