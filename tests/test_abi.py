@@ -136,6 +136,23 @@ def test_validation_errors(capi, kw, status):
     assert len(capi.lib().mppi_last_error()) > 0
 
 
+def test_quadrotor_negative_position_weight_rejected(capi):
+    """The rollout folds sqrt(w) into the position differences, so w_xy, w_z < 0 are refused
+    (include/mppi.h, mppi_quadrotor_cost_t) -- before any device is touched."""
+    from paper_1509_01149_b200.plants import PlantSpec
+    for field in ("w_xy", "w_z"):
+        spec = PlantSpec("quadrotor")
+        setattr(spec.cost.p.quadrotor, field, -1.0)
+        S = np.ascontiguousarray(np.eye(4) * 0.005)
+        Rm = np.ascontiguousarray(np.eye(4))
+        ctx = C.c_void_p()
+        st = capi.lib().mppi_create(C.byref(spec.dyn), C.byref(spec.cost), 256, 10, 0.02, 5e-3, 1.0, 4,
+                                    S.ctypes.data_as(C.POINTER(C.c_double)),
+                                    Rm.ctypes.data_as(C.POINTER(C.c_double)), None, None, C.byref(ctx))
+        assert st == 1 and not ctx.value
+        assert b"w_xy and w_z" in capi.lib().mppi_last_error()
+
+
 def test_dist_validation(capi):
     st, _ = _create(capi, K=256, dist=capi.dist_t(2, 2))
     assert st == 1
