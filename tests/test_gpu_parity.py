@@ -99,6 +99,12 @@ def test_costs_c3_racecar(oracle):
     _costs_parity(oracle, w, 4096, max_excluded=0.05)
 
 
+def test_costs_c3_racecar_every_sample(oracle):
+    """C3 at its full size (K = 16384, T = 150), every sample against the oracle."""
+    w = get("C3")
+    _costs_parity(oracle, w, w.K, max_excluded=0.01)
+
+
 def test_costs_c4_quadrotor(oracle):
     w = get("C4")
     _costs_parity(oracle, w, 4096, max_excluded=0.05)
