@@ -61,3 +61,37 @@ def test_reference_arm_json_line():
     assert line["config"]["workload"].startswith("C1: cartpole K=256 T=50")
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_rollout_roofline_arithmetic():
+    """achieved = FLOP/ss x K T / time; issue fraction from the instruction count; the ceiling of
+    the instruction mix from the FMA-heavy pipe utilisation of the same capture."""
+    consts = {"x2-grid-fused-epi:quadrotor": {"flop": 340.0, "inst": 300.0, "dram_bytes": 28.0,
+                                              "fmaheavy_pipe_pct": 72.0, "capture": "c5_epi"}}
+    r = bench.rollout_roofline("x2-grid-fused-epi", "quadrotor", 1 << 22, 200, 10.0, 74.4, 148, 1965.0,
+                               consts, {"stale": False})
+    units = (1 << 22) * 200
+    assert abs(r["achieved"] - 340.0 * units / 10e-3 / 1e12) < 1e-9
+    assert abs(r["frac"] - r["achieved"] / 74.4) < 1e-12
+    assert abs(r["issue_frac"] - 300.0 / 32 * units / 10e-3 / (148 * 4 * 1965e6)) < 1e-12
+    assert abs(r["frac_ceiling_of_mix"] - r["frac"] / 0.72) < 1e-12
+    assert r["traffic"] == 28.0 * units and r["bound"] == "alu"
+    # a variant without constants reports no fraction rather than a wrong one
+    r = bench.rollout_roofline("scalar:cartpole", "cartpole", 256, 50, 0.01, 74.4, 148, 1965.0, consts, {})
+    assert r["frac"] is None and "no ncu constants" in r["note"]
+
+
+def test_roofline_constants_staleness(tmp_path, monkeypatch):
+    """bench.py marks the committed constants stale when the rollout machine code they were keyed
+    to is not the library's."""
+    import json
+    p = tmp_path / "rc.json"
+    p.write_text(json.dumps({"source_hash": "0000", "variants": {"v:p": {"flop": 1.0}}}))
+    monkeypatch.setattr(bench, "CONSTANTS_PATH", str(p))
+    from paper_1509_01149_b200 import build as B
+    monkeypatch.setattr(B, "source_hash", lambda lib=None: "1111")
+    v, meta = bench.roofline_constants()
+    assert v == {"v:p": {"flop": 1.0}} and meta["stale"] is True
+    monkeypatch.setattr(B, "source_hash", lambda lib=None: "0000")
+    v, meta = bench.roofline_constants()
+    assert meta["stale"] is False
