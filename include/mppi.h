@@ -316,7 +316,7 @@ typedef enum {
                                           bit-identical to the separate pass, and the per-t CTA
                                           minima) and the per-(CTA, t) weighted sums in their
                                           epilogue, rescaled to S_min,t afterwards (default 1) */
-    MPPI_OPTION_GATHER_COMBINE = 9,    /* sharded step with the library's communicator, trajectory
+    MPPI_OPTION_GATHER_COMBINE = 9     /* sharded step with the library's communicator, trajectory
                                           weights: ONE collective instead of two -- every rank forms
                                           its weighted sums against its own minimum, an ncclAllGather
                                           exchanges the [key, eta_r, A_r] records, and every rank
@@ -324,12 +324,6 @@ typedef enum {
                                           (PAPER.md:320 is invariant to the shift).  k* and S_min
                                           identical, U equal to rounding (single rank: bitwise)
                                           (default 1) */
-    MPPI_OPTION_WARP_SPECIALIZED = 10  /* packed quadrotor path with in-kernel noise and the fused
-                                          reduction at small K (K_loc a multiple of 256, <= 131072):
-                                          256-thread CTAs whose second half draws the noise into a
-                                          shared-memory ring for the first half's rollouts
-                                          (producer/consumer named barriers); bitwise identical
-                                          results (default 1) */
 } mppi_option_t;
 
 /* mppi_set_option — execution options that never change results (FUSED_REDUCTION: U to rounding). */

@@ -38,7 +38,6 @@ constexpr int kNoiseTT = 8;  // timesteps per noise thread
 constexpr int kMaxStaticPairs = 32;
 // the two-samples-per-thread quadrotor kernel is used from this many samples per GPU on (below
 // it the one-sample kernel fills the 148 SMs better: scripts/compare_pack.py on B200)
-constexpr int64_t kWsMaxK = 131072;      // warp-specialised packed rollout up to here (MPPI_OPTION_WARP_SPECIALIZED)
 constexpr int64_t kPackedMinK = 65536;  // quadrotor: obstacle pairs compiled as a constant up to here
 
 // per-timestep constants of the rollout staged in shared memory (one 48-byte record per t)
@@ -164,7 +163,6 @@ struct Ctx {
     float* d_grec = nullptr;              // one-collective combine: this rank's record [gather_record_len]
     float* d_gather = nullptr;            // and every rank's, [world][gather_record_len]
     bool gather_combine = true;           // MPPI_OPTION_GATHER_COMBINE
-    bool use_ws = true;                   // MPPI_OPTION_WARP_SPECIALIZED (small K)
 };
 
 // Launch (or collect, see Ctx::collect) one kernel whose single parameter is `args`.

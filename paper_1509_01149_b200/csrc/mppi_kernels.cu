@@ -49,19 +49,6 @@ __device__ __forceinline__ void store_eps(float* p, const float* z) {
 // advance writes U before the next step's rollout, uses ordinary edges).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
-// Named CTA barriers (the warp-specialised rollout's producer/consumer ring; id 0 is __syncthreads):
-// bar.arrive orders the caller's earlier shared/global writes before the release of the threads
-// that bar.sync on the same id, without waiting itself.
-constexpr int kWsStages = 4;                  // ring depth (a power of two)
-constexpr int kWsBarFull = 1;                 // ids 1..4: slot s filled
-constexpr int kWsBarEmpty = 1 + kWsStages;    // ids 5..8: slot s consumed
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
 // Per-thread asynchronous copy of one noise element group (4m bytes) into shared memory
 // (LDGSTS: cp.async, non-blocking, no register tied to the load).  dst: shared-window address.
 template <int M>
@@ -495,18 +482,9 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
 // tile (written moments ago) to form eta_c and A_c[t][j]; the HBM stream of that read overlaps
 // the other CTAs' ALU-bound rollouts instead of running as a separate pass.  epi_combine_kernel
 // rescales by exp(-(m_c - S_min)/lambda) (the online-softmax identity) in a fixed order.
-//
-// WS (warp-specialised, small K; GEN + DIAG + EPI only, K_loc a multiple of 256): 256 threads per
-// CTA for the same 256 samples -- threads 0..127 run the rollouts (as above), threads 128..255 are
-// noise producers, thread j + 128 drawing the noise of thread j's two samples step by step into a
-// kWsStages-deep shared-memory ring (named barriers FULL(s) / EMPTY(s)) and to eps_out.  The
-// rollout threads' step loop loses the ~40 % of its instructions the noise contract costs; with
-// few samples per SM (K <= 2^17) that shortens the step loop's critical path instead of
-// competing for issue slots that are already full at large K.
-template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true, bool EPI = false, bool WS = false>
-__global__ void __launch_bounds__(WS ? 2 * kRolloutThreads : kRolloutThreads, WS ? 2 : MPPI_X2_MINB)
+template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true, bool EPI = false>
+__global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
     rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
-    static_assert(!WS || (GEN && DIAG && EPI && !QSTEP), "warp-specialised: the C5-type variant only");
     constexpr int M = 4;
     extern __shared__ float4 smem4[];
     float4* sObs = smem4;
@@ -519,14 +497,6 @@ __global__ void __launch_bounds__(WS ? 2 * kRolloutThreads : kRolloutThreads, WS
     // load is one LDS with an immediate base, no address arithmetic)
     __shared__ float sCentXY[NP == kCellGrid ? 2 * kCellMaxCent : 1];
     const int tid = threadIdx.x;
-    // WS: producer threads (tid >= 128) and the rollout-thread index both groups share
-    const bool prod = WS && tid >= kRolloutThreads;
-    const int ltid = WS ? (tid & (kRolloutThreads - 1)) : tid;
-    // WS ring [kWsStages][128 threads][2 samples] float4, after the cell table (16-B aligned)
-    float4* sWs = nullptr;
-    if constexpr (WS)
-        sWs = reinterpret_cast<float4*>(
-            (reinterpret_cast<uintptr_t>(sCells + (NP == kCellGrid ? a.cell_nx * a.cell_ny : 0)) + 15) & ~uintptr_t(15));
     // (DIAG keeps its own staging, in this order: the shared helper, or another order, costs
     // the hot loop 4 % through ptxas' register allocation)
     if constexpr (DIAG) {
@@ -567,33 +537,10 @@ __global__ void __launch_bounds__(WS ? 2 * kRolloutThreads : kRolloutThreads, WS
     __syncthreads();
     pdl_wait();
 
-    const int k = 2 * (blockIdx.x * (WS ? kRolloutThreads : blockDim.x) + ltid);   // samples k, k+1
+    const int k = 2 * (blockIdx.x * blockDim.x + tid);                 // samples k, k+1
     long long key = LLONG_MAX;
     float cost_a = 0.0f, cost_b = 0.0f;                                // (EPI)
-    if constexpr (WS) {
-        if (prod) {   // noise producer of samples k, k+1 (every k is valid: K_loc % 256 == 0)
-            const unsigned kg = a.k_offset + (unsigned)k;
-            float4* op = reinterpret_cast<float4*>(a.eps_out + (size_t)k * M);
-            const size_t row4 = (size_t)a.K_loc * M / 4;
-            for (int t = 0; t < a.T; ++t) {
-                const int slot = t & (kWsStages - 1);
-                if (t >= kWsStages) named_bar_sync(kWsBarEmpty + slot, 2 * kRolloutThreads);
-                float ea[4], eb[4];
-                bm32_normals_x2<4>(philox4x32_10_dev(kg, (unsigned)t, a.step_lo, a.step_hi, a.keys),
-                                   philox4x32_10_dev(kg + 1u, (unsigned)t, a.step_lo, a.step_hi, a.keys), ea, eb);
-                const float4 za = make_float4(ea[0], ea[1], ea[2], ea[3]);
-                const float4 zb = make_float4(eb[0], eb[1], eb[2], eb[3]);
-                float4* sl = sWs + (slot * kRolloutThreads + ltid) * 2;
-                sl[0] = za;
-                sl[1] = zb;
-                op[0] = za;
-                op[1] = zb;
-                op += row4;
-                named_bar_arrive(kWsBarFull + slot, 2 * kRolloutThreads);
-            }
-        }
-    }
-    if (!prod && k < a.K_loc) {
+    if (k < a.K_loc) {
         QuadrotorX2 st;
         st.load(a.x0_dev ? a.x0_dev : a.x0);
         ObstacleView ob{NP >= 0 ? a.obs_k : sObs, a.n_obs_pairs};
@@ -689,16 +636,7 @@ __global__ void __launch_bounds__(WS ? 2 * kRolloutThreads : kRolloutThreads, WS
         MPPI_UNROLL_(MPPI_X2_UNROLL)
         for (int t = 0; t < a.T; ++t, ++rec) {
             float ea[4], eb[4];
-            if constexpr (WS) {
-                // the producer thread's values for this step (FULL), then release the slot (EMPTY)
-                const int slot = t & (kWsStages - 1);
-                named_bar_sync(kWsBarFull + slot, 2 * kRolloutThreads);
-                const float4* sl = sWs + (slot * kRolloutThreads + ltid) * 2;
-                const float4 za = sl[0], zb = sl[1];
-                ea[0] = za.x; ea[1] = za.y; ea[2] = za.z; ea[3] = za.w;
-                eb[0] = zb.x; eb[1] = zb.y; eb[2] = zb.z; eb[3] = zb.w;
-                if (t + kWsStages < a.T) named_bar_arrive(kWsBarEmpty + slot, 2 * kRolloutThreads);
-            } else if constexpr (GEN) {
+            if constexpr (GEN) {
                 // eps_t enters only the motor-lag derivative and IS_t, late in the step, so it is
                 // drawn in the same iteration and the scheduler overlaps it with the dynamics
                 bm32_normals_x2<4>(philox4x32_10_dev(kg, (unsigned)t, a.step_lo, a.step_hi, a.keys),
@@ -753,7 +691,7 @@ __global__ void __launch_bounds__(WS ? 2 * kRolloutThreads : kRolloutThreads, WS
         cost_b = sb;
     }
     key = warp_min_ll(key);
-    __shared__ long long wmin[(WS ? 2 : 1) * kRolloutThreads / 32];
+    __shared__ long long wmin[kRolloutThreads / 32];
     __shared__ long long sBlockKey;
     if ((tid & 31) == 0) wmin[tid >> 5] = key;
     __syncthreads();
@@ -866,19 +804,16 @@ __global__ void __launch_bounds__(WS ? 2 * kRolloutThreads : kRolloutThreads, WS
         const long long bk = sBlockKey;
         if (bk == LLONG_MAX) return;                                  // no sample in this CTA
         const float mc = key_cost(bk);
-        const bool va = !prod && k < a.K_loc;
+        const bool va = k < a.K_loc;
         const float wa = va ? expf(-__fdiv_rn(cost_a - mc, a.lambda)) : 0.0f;
         const float wb = va ? expf(-__fdiv_rn(cost_b - mc, a.lambda)) : 0.0f;
-        if (!prod) {
-            sW[2 * tid] = wa;
-            sW[2 * tid + 1] = wb;
-        }
+        sW[2 * tid] = wa;
+        sW[2 * tid + 1] = wb;
         const float ew = warp_sum(wa + wb);
-        if (lane == 0 && !prod) sEta[warp] = ew;
+        if (lane == 0) sEta[warp] = ew;
         __syncthreads();
-        if (prod) return;                                             // (WS: no barrier follows)
-        const int k0 = 2 * blockIdx.x * (WS ? kRolloutThreads : blockDim.x);
-        const int nk = min(2 * (WS ? kRolloutThreads : (int)blockDim.x), a.K_loc - k0);
+        const int k0 = 2 * blockIdx.x * blockDim.x;
+        const int nk = min(2 * (int)blockDim.x, a.K_loc - k0);
         float* part = a.epi_part + (size_t)blockIdx.x * (a.T * M + 4);   // [A (T M)][m_c, eta_c, -, -]
         const float* eps_src = GEN ? a.eps_out : a.eps;
         // four sums across the warp in 6 shuffles (transpose-reduce, fixed order): after the
@@ -2081,25 +2016,16 @@ static void fill_rollout_args(Ctx& c, const typename Plant::Params& P, const flo
         a.obs_k[i] = i < c.n_obs_pairs ? c.obs_host[i] : make_float4(-1e15f, -1e15f, -1e15f, -1e15f);
 }
 
-// the warp-specialised packed rollout (MPPI_OPTION_WARP_SPECIALIZED): small K only -- at large K
-// the step is issue-bound and the producers would only take issue slots and registers
-static bool ws_applies(const Ctx& c) {
-    return c.use_ws && c.K_loc % (2 * kRolloutThreads) == 0 && c.K_loc <= kWsMaxK &&
-           rollout_smem_bytes(c, true) + 16 + (size_t)kWsStages * kRolloutThreads * 2 * sizeof(float4) +
-                   kRolloutStaticSmem <= smem_optin_bytes();
-}
-
 template <class Plant, bool DIAG, int NP, bool X2 = false>
 static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, const float* x0,
                                     const float* U, const float* eps, float* costs_out) {
     RolloutArgs<typename Plant::Params> a{};
     fill_rollout_args<Plant>(c, P, x0, U, eps, costs_out, a);
     const int spt = X2 ? 2 : 1;                                      // samples per thread
-    size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
-                  (c.gen_eps ? 0 : (size_t)(X2 ? 2 : kEpsStages) * kRolloutThreads * spt * Plant::M * sizeof(float)) +
-                  (DIAG ? 0 : (size_t)c.T * 2 * Plant::M * Plant::M * sizeof(float)) +
-                  (NP == kCellGrid ? c.cent_host.size() * sizeof(float2) + c.cells_host.size() * sizeof(uint32_t) : 0);
-    int threads = kRolloutThreads;
+    const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
+                        (c.gen_eps ? 0 : (size_t)(X2 ? 2 : kEpsStages) * kRolloutThreads * spt * Plant::M * sizeof(float)) +
+                        (DIAG ? 0 : (size_t)c.T * 2 * Plant::M * Plant::M * sizeof(float)) +
+                        (NP == kCellGrid ? c.cent_host.size() * sizeof(float2) + c.cells_host.size() * sizeof(uint32_t) : 0);
     const void* kern;
     if constexpr (X2 && !DIAG) {   // general Sigma / A_t: grid path only
         static_assert(NP == kCellGrid, "packed general-Sigma kernel: candidate-grid path only");
@@ -2141,11 +2067,6 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
                     a.epi_part = c.d_epi;
                     a.lambda = c.lambda;
                     kern = (const void*)rollout_kernel_x2<NP, true, false, true, true>;
-                    if (ws_applies(c)) {   // small K: noise-producer warps beside the rollout warps
-                        kern = (const void*)rollout_kernel_x2<NP, true, false, true, true, true>;
-                        threads = 2 * kRolloutThreads;
-                        smem += 16 + (size_t)kWsStages * kRolloutThreads * 2 * sizeof(float4);
-                    }
                 } else {
                     kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
                 }
@@ -2174,7 +2095,7 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
         if (e != cudaSuccess) return e;
     }
     const unsigned grid = (unsigned)((c.K_loc / spt + kRolloutThreads - 1) / kRolloutThreads);
-    return emit(c, (const void*)kern, dim3(grid), dim3(threads), smem, &a, sizeof(a),
+    return emit(c, (const void*)kern, dim3(grid), dim3(kRolloutThreads), smem, &a, sizeof(a),
                 MPPI_KERNEL_ROLLOUT);
 }
 

@@ -730,7 +730,6 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
         case MPPI_OPTION_SPARSE_REDUCTION: ctx->c.sparse_wsum = value != 0; return MPPI_OK;
         case MPPI_OPTION_FUSED_REDUCTION: ctx->c.epi = value != 0; return MPPI_OK;
         case MPPI_OPTION_GATHER_COMBINE: ctx->c.gather_combine = value != 0; return MPPI_OK;
-        case MPPI_OPTION_WARP_SPECIALIZED: ctx->c.use_ws = value != 0; return MPPI_OK;
         case MPPI_OPTION_PDL:
             MPPI_CUDA(cudaStreamSynchronize(ctx->c.stream), "stream sync");
             ctx->c.use_pdl = value != 0;

@@ -795,30 +795,3 @@ def test_fused_reduction_long_horizon(weighting):
     torch.testing.assert_close(Ua, Ub, rtol=1e-5, atol=1e-6)
     a.close()
     b.close()
-
-
-@pytest.mark.parametrize("K,lam", [(65536, None), (65536, 30.0), (1 << 17, None)])
-def test_warp_specialized_rollout_is_bitwise(K, lam):
-    """MPPI_OPTION_WARP_SPECIALIZED (small K): noise-producer warps fill a shared-memory ring for
-    the rollout warps; costs, key, noise written for the reduction and the fused-reduction update
-    are bit for bit those of the single-group kernel, step after step, graph and direct launches."""
-    from paper_1509_01149_b200 import _capi as A
-    w = get("C4")
-    if lam is not None:
-        w.lam = lam
-    a = from_workload(w, K=K)
-    b = from_workload(w, K=K)
-    b.set_option(A.MPPI_OPTION_WARP_SPECIALIZED, 0)
-    for graph in (True, False):
-        a.use_graph(graph)
-        b.use_graph(graph)
-        Ua, Ub = cuda_u(w), cuda_u(w)
-        for i in range(3):
-            a.optimize(w.x0, Ua, 6, i)
-            b.optimize(w.x0, Ub, 6, i)
-            assert any("rollout_kernel_x2ILin2ELb1ELb0ELb1ELb1ELb1E" in n for n in a.last_kernels()), a.last_kernels()
-            assert not any("ELb1ELb1ELb1E" in n for n in b.last_kernels())
-            torch.cuda.synchronize()
-            assert torch.equal(Ua, Ub) and a.stats() == b.stats()
-    a.close()
-    b.close()
