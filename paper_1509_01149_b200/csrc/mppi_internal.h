@@ -157,6 +157,7 @@ struct Ctx {
     bool x0_on_device = false;            // launch_rollout's x0 is a device pointer (closed loop)
     std::vector<KLaunch> pending;
     GraphState graphs[2];
+    GraphState loop_graph;                // mppi_closed_loop's n-step graph, reused while its kernel sequence is unchanged
     // row (e): a communicator the library drives itself (mppi_nccl_attach)
     void* nccl = nullptr;                 // ncclComm_t
     float* d_commbuf = nullptr;           // [T + T*m]: [eta, A] (trajectory: 1 + T*m used) all-reduced across ranks

@@ -307,15 +307,19 @@ mppi_status_t digest_params(Ctx& c, const mppi_dynamics_t* d, const mppi_cost_t*
     }
 }
 
+void free_graph(GraphState& G) {
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    if (G.graph) cudaGraphDestroy(G.graph);
+    G.exec = nullptr;
+    G.graph = nullptr;
+    G.nodes.clear();
+    G.funcs.clear();
+    G.last.clear();
+}
+
 void free_graphs(Ctx& c) {
-    for (GraphState& G : c.graphs) {
-        if (G.exec) cudaGraphExecDestroy(G.exec);
-        if (G.graph) cudaGraphDestroy(G.graph);
-        G.exec = nullptr;
-        G.graph = nullptr;
-        G.nodes.clear();
-        G.funcs.clear();
-    }
+    for (GraphState& G : c.graphs) free_graph(G);
+    free_graph(c.loop_graph);
 }
 
 void free_ctx(Ctx& c) {
@@ -1173,22 +1177,41 @@ mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed,
     c.x0_on_device = false;
     if (e != cudaSuccess) return cuda_fail(e, "collecting the closed loop");
     if (x_log) MPPI_CUDA(cudaMemcpyAsync(x_log, x, (size_t)c.n * sizeof(float), cudaMemcpyDeviceToDevice, c.stream), "x_log[0]");
-    cudaGraph_t g = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    MPPI_CUDA(cudaGraphCreate(&g, 0), "cudaGraphCreate");
-    cudaGraphNode_t prev = nullptr;
-    for (KLaunch& L : c.pending) {
-        cudaKernelNodeParams p = node_params(L);
-        cudaGraphNode_t node;
-        cudaError_t ee = cudaGraphAddKernelNode(&node, g, prev ? &prev : nullptr, prev ? 1 : 0, &p);
-        if (ee != cudaSuccess) { cudaGraphDestroy(g); return cuda_fail(ee, "closed-loop graph"); }
-        prev = node;
+    // the instantiated loop graph is kept: a later call with the same kernel sequence (same
+    // n_steps and variants) only updates the nodes whose arguments changed (seed, step, pointers)
+    GraphState& G = c.loop_graph;
+    bool same = G.exec && G.funcs.size() == c.pending.size();
+    for (size_t i = 0; same && i < c.pending.size(); ++i) same = G.funcs[i] == c.pending[i].func;
+    if (!same) {
+        free_graph(G);
+        MPPI_CUDA(cudaGraphCreate(&G.graph, 0), "cudaGraphCreate");
+        cudaGraphNode_t prev = nullptr;
+        for (KLaunch& L : c.pending) {
+            cudaKernelNodeParams p = node_params(L);
+            cudaGraphNode_t node;
+            cudaError_t ee = cudaGraphAddKernelNode(&node, G.graph, prev ? &prev : nullptr, prev ? 1 : 0, &p);
+            if (ee != cudaSuccess) { free_graph(G); return cuda_fail(ee, "closed-loop graph"); }
+            G.nodes.push_back(node);
+            G.funcs.push_back(L.func);
+            G.last.push_back(L);
+            prev = node;
+        }
+        e = cudaGraphInstantiate(&G.exec, G.graph, 0);
+        if (e != cudaSuccess) { free_graph(G); return cuda_fail(e, "closed-loop graph instantiate"); }
+    } else {
+        for (size_t i = 0; i < c.pending.size(); ++i) {
+            KLaunch& L = c.pending[i];
+            const KLaunch& O = G.last[i];
+            if (L.nargs == O.nargs && memcmp(L.args, O.args, L.nargs) == 0 && L.smem == O.smem &&
+                L.grid.x == O.grid.x && L.grid.y == O.grid.y && L.grid.z == O.grid.z && L.block.x == O.block.x)
+                continue;
+            cudaKernelNodeParams p = node_params(L);
+            MPPI_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, G.nodes[i], &p), "closed-loop graph node update");
+            G.last[i] = L;
+        }
     }
-    e = cudaGraphInstantiate(&exec, g, 0);
-    if (e == cudaSuccess) e = cudaGraphLaunch(exec, c.stream);
+    e = cudaGraphLaunch(G.exec, c.stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
-    if (exec) cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(g);
     if (e != cudaSuccess) return cuda_fail(e, "closed-loop graph launch");
     return MPPI_OK;
 }

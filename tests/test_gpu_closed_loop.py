@@ -187,3 +187,24 @@ def test_device_loop_tracks_oracle_closed_loop(oracle, cfg, K):
     assert np.allclose(xl, xs, rtol=1e-4, atol=1e-5), np.max(np.abs(xl - xs))
     assert np.allclose(ql.cpu().numpy(), qs, rtol=1e-4, atol=1e-4)
     g.close()
+
+
+def test_closed_loop_graph_reuse_equals_fresh_context():
+    """A second mppi_closed_loop call of the same length reuses the instantiated loop graph with
+    updated node arguments (seed, step, pointers): bitwise the results of a fresh context."""
+    w = get("C2")
+    w.K = 1024
+    a = from_workload(w)
+    b = from_workload(w)
+    n = 6
+    x, U = torch.tensor(w.x0, device="cuda"), torch.tensor(w.U0, device="cuda")
+    a.closed_loop(x, U, n, seed=3, step0=0, u_init=np.zeros(w.m))          # builds the graph
+    outs = []
+    for m in (a, b):                                                       # a reuses, b builds
+        x, U = torch.tensor(w.x0, device="cuda"), torch.tensor(w.U0, device="cuda")
+        xl, ul, ql = m.closed_loop(x, U, n, seed=5, step0=40, u_init=np.zeros(w.m))
+        outs.append((xl.cpu().numpy(), ul.cpu().numpy(), ql.cpu().numpy(), U.cpu().numpy()))
+    for u, v in zip(outs[0], outs[1]):
+        assert np.array_equal(u, v)
+    a.close()
+    b.close()
