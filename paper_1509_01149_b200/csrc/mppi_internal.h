@@ -207,6 +207,7 @@ int nccl_min_key(Ctx& c, long long* key);
 int nccl_min_f32(Ctx& c, float* buf, size_t count);
 int nccl_sum_buf(Ctx& c, float* buf, size_t count);
 int nccl_all_gather(Ctx& c, const float* send, float* recv, size_t count);   // recv: [world][count]
+int nccl_async_error(Ctx& c);             // nonzero: the communicator reported an asynchronous error
 int nccl_sum_f64(Ctx& c, double* buf, size_t count);
 cudaError_t launch_fk_reduce(Ctx& c, double* part, int nblk);   // Feynman-Kac partial sums
 cudaError_t launch_ctg(Ctx& c);                                  // cost-to-go + per-t minima

@@ -23,6 +23,7 @@ struct NcclApi {
     decltype(&ncclAllGather) all_gather = nullptr;
     decltype(&ncclCommDestroy) comm_destroy = nullptr;
     decltype(&ncclGetErrorString) error_string = nullptr;
+    decltype(&ncclCommGetAsyncError) async_error = nullptr;   // optional
     bool ok = false;
 };
 
@@ -38,6 +39,7 @@ const NcclApi& api() {
         r.all_gather = (decltype(r.all_gather))dlsym(h, "ncclAllGather");
         r.comm_destroy = (decltype(r.comm_destroy))dlsym(h, "ncclCommDestroy");
         r.error_string = (decltype(r.error_string))dlsym(h, "ncclGetErrorString");
+        r.async_error = (decltype(r.async_error))dlsym(h, "ncclCommGetAsyncError");
         r.ok = r.get_unique_id && r.comm_init_rank && r.all_reduce && r.all_gather && r.comm_destroy && r.error_string;
         return r;
     }();
@@ -73,6 +75,15 @@ int nccl_attach(Ctx& c, const unsigned char* id_bytes) {
 void nccl_detach(Ctx& c) {
     if (c.nccl && api().ok) api().comm_destroy((ncclComm_t)c.nccl);
     c.nccl = nullptr;
+}
+
+// an asynchronous communicator error (a failed peer, a network fault) as an NCCL result code; 0
+// while the communicator is healthy or when the symbol is unavailable
+int nccl_async_error(Ctx& c) {
+    if (!c.nccl || !api().ok || !api().async_error) return 0;
+    ncclResult_t r = ncclSuccess;
+    if (api().async_error((ncclComm_t)c.nccl, &r) != ncclSuccess) return 0;
+    return (r == ncclSuccess || r == ncclInProgress) ? 0 : (int)r;
 }
 
 const char* nccl_error(int r) { return api().ok && r > 0 ? api().error_string((ncclResult_t)r) : "NCCL unavailable"; }

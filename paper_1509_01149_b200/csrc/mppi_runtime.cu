@@ -371,12 +371,15 @@ mppi_status_t check_ctx(const mppi_ctx* ctx) {
     return MPPI_OK;
 }
 
-// Surface asynchronous faults of earlier work before enqueuing more.
+// Surface asynchronous faults of earlier work before enqueuing more (CUDA, and an attached NCCL
+// communicator's asynchronous error state).
 mppi_status_t sticky_check(Ctx& c) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "earlier CUDA error");
     e = cudaStreamQuery(c.stream);
     if (e != cudaSuccess && e != cudaErrorNotReady) return cuda_fail(e, "stream fault");
+    if (const int r = nccl_async_error(c))
+        return fail(MPPI_ERR_NCCL, "NCCL communicator error: %s", nccl_error(r));
     return MPPI_OK;
 }
 
