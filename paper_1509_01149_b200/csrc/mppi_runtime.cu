@@ -770,23 +770,23 @@ static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t s
             MPPI_CUDA(launch_wsum(c, eps, &c.d_stats->min_key), "wsum_kernel launch");
         }
         MPPI_CUDA(launch_finalize_record(c, c.d_grec), "finalize (record) launch");
-        { ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_all_gather(c, c.d_grec, c.d_gather, (size_t)gather_record_len(c)); }
+        { NvtxRange nv_("nccl collective"); ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_all_gather(c, c.d_grec, c.d_gather, (size_t)gather_record_len(c)); }
         if (r) return fail(MPPI_ERR_NCCL, "ncclAllGather(records): %s", nccl_error(r));
         MPPI_CUDA(launch_finalize_gathered(c, c.d_gather, c.world, U), "finalize (gathered) launch");
         c.last_eps = eps;
         return MPPI_OK;
     }
-    { ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_min_key(c, &c.d_stats->min_key); }
+    { NvtxRange nv_("nccl collective"); ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_min_key(c, &c.d_stats->min_key); }
     if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(MIN key): %s", nccl_error(r));
     if (c.ctg) {
         // NEXT-1 sharded: local suffix sums and per-t minima -> MIN over the T
         // minima -> per-(t, k) weights and local sums -> SUM of [eta_t (T), A (T m)] -> update
         MPPI_CUDA(launch_ctg(c), "cost-to-go launch");
-        { ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_min_f32(c, c.d_ctg_smin, (size_t)c.T); }
+        { NvtxRange nv_("nccl collective"); ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_min_f32(c, c.d_ctg_smin, (size_t)c.T); }
         if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(MIN S_t): %s", nccl_error(r));
         MPPI_CUDA(launch_wsum_ctg(c, eps), "wsum_ctg launch");
         MPPI_CUDA(launch_finalize_ctg(c, nullptr, nullptr, c.d_commbuf), "finalize_ctg (partials) launch");
-        { ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_sum_buf(c, c.d_commbuf, (size_t)c.T + (size_t)c.T * c.m); }
+        { NvtxRange nv_("nccl collective"); ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_sum_buf(c, c.d_commbuf, (size_t)c.T + (size_t)c.T * c.m); }
         if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(SUM [eta_t, A]): %s", nccl_error(r));
         MPPI_CUDA(launch_finalize_ctg(c, U, c.d_commbuf, nullptr), "finalize_ctg (apply) launch");
         c.last_eps = eps;
@@ -798,7 +798,7 @@ static mppi_status_t optimize_nccl(Ctx& c, const float* x0, float* U, uint64_t s
         MPPI_CUDA(launch_wsum(c, eps, &c.d_stats->min_key), "wsum_kernel launch");
     }
     MPPI_CUDA(launch_finalize(c, nullptr, c.d_commbuf, nullptr), "finalize (partials) launch");
-    { ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_sum_buf(c, c.d_commbuf, (size_t)1 + (size_t)c.T * c.m); }
+    { NvtxRange nv_("nccl collective"); ProfScope p(c, MPPI_KERNEL_COLLECTIVE); r = nccl_sum_buf(c, c.d_commbuf, (size_t)1 + (size_t)c.T * c.m); }
     if (r) return fail(MPPI_ERR_NCCL, "ncclAllReduce(SUM [eta, A]): %s", nccl_error(r));
     MPPI_CUDA(launch_finalize(c, c.d_commbuf, nullptr, U), "finalize (apply) launch");
     c.last_eps = eps;
