@@ -174,22 +174,28 @@ void noise_one(uint64_t seed, uint64_t step, uint32_t t, uint32_t k, float z[4])
 // ---------------------------------------------------------------------------
 struct MathD {
     typedef double S;
+    static constexpr bool kFma = false;
     static S sin(S x) { return std::sin(x); }
     static S cos(S x) { return std::cos(x); }
     static S atan(S x) { return std::atan(x); }
     static S exp(S x) { return std::exp(x); }
     static S sqrt(S x) { return std::sqrt(x); }
 };
-struct MathF {  // twin 1: fp32 libm
+struct MathF {  // twin 1: fp32 libm, plain operations (no contraction: -ffp-contract=off)
     typedef float S;
+    static constexpr bool kFma = false;
     static S sin(S x) { return std::sin(x); }
     static S cos(S x) { return std::cos(x); }
     static S atan(S x) { return std::atan(x); }
     static S exp(S x) { return std::exp(x); }
     static S sqrt(S x) { return std::sqrt(x); }
 };
-struct MathFviaD {  // twin 2: fp32 state, transcendentals evaluated in fp64 then rounded
+// twin 2: fp32 state, transcendentals evaluated in fp64 then rounded, and
+// explicit fmaf in the Euler and cost updates (kFma) -- a rounding sequence independent of
+// twin 1's, so that the two twins sample the fp32 divergence of a rollout twice
+struct MathFviaD {
     typedef float S;
+    static constexpr bool kFma = true;
     static S sin(S x) { return (float)std::sin((double)x); }
     static S cos(S x) { return (float)std::cos((double)x); }
     static S atan(S x) { return (float)std::atan((double)x); }
@@ -198,6 +204,14 @@ struct MathFviaD {  // twin 2: fp32 state, transcendentals evaluated in fp64 the
 };
 
 template <class S> S clampv(S v, S lo, S hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// a b + c: one fused rounding in twin 2 (M::kFma), the plain two roundings otherwise (the fp64
+// reference and twin 1 keep their original operation sequence bit for bit)
+template <class M>
+typename M::S mad(typename M::S a, typename M::S b, typename M::S c) {
+    if constexpr (M::kFma) return std::fma(a, b, c);
+    else return a * b + c;
+}
 
 enum { PLANT_CARTPOLE = 1, PLANT_RACECAR = 2, PLANT_QUADROTOR = 3, PLANT_LINEAR = 4 };
 
@@ -250,6 +264,8 @@ template <class M>
 typename M::S cartpole_cost(const double* P, const typename M::S* x) {
     typedef typename M::S S;
     S c = (S)1 + M::cos(x[2]);
+    if constexpr (M::kFma)
+        return mad<M>((S)P[6] * x[1], x[1], mad<M>((S)P[5] * x[3], x[3], mad<M>((S)P[4] * c, c, (S)P[3] * x[0] * x[0])));
     return (S)P[3] * x[0] * x[0] + (S)P[4] * c * c + (S)P[5] * x[3] * x[3] +
            (S)P[6] * x[1] * x[1];
 }
@@ -290,8 +306,12 @@ typename M::S racecar_cost(const double* P, const typename M::S* x) {
     typedef typename M::S S;
     S a = (S)P[15], b = (S)P[16];
     S ex = x[0] / a, ey = x[1] / b;
-    S d = std::fabs(ex * ex + ey * ey - (S)1);
     S dv = x[3] - (S)P[19];
+    if constexpr (M::kFma) {
+        S d = std::fabs(mad<M>(ex, ex, mad<M>(ey, ey, -(S)1)));
+        return mad<M>((S)P[18] * dv, dv, (S)P[17] * d * d);
+    }
+    S d = std::fabs(ex * ex + ey * ey - (S)1);
     return (S)P[17] * d * d + (S)P[18] * dv * dv;
 }
 
@@ -354,6 +374,13 @@ template <class M>
 typename M::S quad_cost(const double* P, const typename M::S* x, typename M::S d, int crashed) {
     typedef typename M::S S;
     S ex = x[0] - (S)P[11], ey = x[1] - (S)P[12], ez = x[2] - (S)P[13];
+    if constexpr (M::kFma) {
+        S q = mad<M>((S)P[15] * ez, ez, mad<M>((S)P[14] * ey, ey, (S)P[14] * ex * ex));
+        q = mad<M>((S)P[16] * x[8], x[8], q);
+        q = mad<M>((S)P[17], mad<M>(x[3], x[3], mad<M>(x[4], x[4], x[5] * x[5])), q);
+        q = mad<M>((S)P[18], M::exp(-d / (S)P[19]), q);
+        return q + (S)P[20] * (S)(crashed ? 1 : 0);
+    }
     S q = (S)P[14] * ex * ex + (S)P[14] * ey * ey + (S)P[15] * ez * ez;
     q += (S)P[16] * x[8] * x[8];
     q += (S)P[17] * (x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
@@ -400,16 +427,16 @@ typename M::S plant_step(const oracle_problem* pb, typename M::S* x, const typen
     switch (pb->plant) {
         case PLANT_CARTPOLE:
             cartpole_deriv<M>(pb->params, x, v, xd);
-            for (int i = 0; i < n; ++i) x[i] = x[i] + xd[i] * dt;
+            for (int i = 0; i < n; ++i) x[i] = mad<M>(xd[i], dt, x[i]);   // x + F dt
             return cartpole_cost<M>(pb->params, x);
         case PLANT_RACECAR:
             racecar_deriv<M>(pb->params, x, v, xd);
-            for (int i = 0; i < n; ++i) x[i] = x[i] + xd[i] * dt;
+            for (int i = 0; i < n; ++i) x[i] = mad<M>(xd[i], dt, x[i]);   // x + F dt
             return racecar_cost<M>(pb->params, x);
         case PLANT_QUADROTOR: {
             if (!*crashed) {  // "the rollout stops simulating the dynamics" once C = 1
                 quad_deriv<M>(pb->params, x, v, xd);
-                for (int i = 0; i < n; ++i) x[i] = x[i] + xd[i] * dt;
+                for (int i = 0; i < n; ++i) x[i] = mad<M>(xd[i], dt, x[i]);   // x + F dt
             }
             S d = quad_obstacle_distance<M>(pb, x);
             if (x[2] <= (S)pb->params[21] || d <= (S)0) *crashed = 1;  // sticky
@@ -418,7 +445,7 @@ typename M::S plant_step(const oracle_problem* pb, typename M::S* x, const typen
         case PLANT_LINEAR:
         default:
             linear_deriv<M>(pb, x, v, xd);
-            for (int i = 0; i < n; ++i) x[i] = x[i] + xd[i] * dt;
+            for (int i = 0; i < n; ++i) x[i] = mad<M>(xd[i], dt, x[i]);   // x + F dt
             return linear_cost<M>(pb, x);
     }
 }
@@ -525,7 +552,7 @@ double rollout_one(const oracle_problem* pb, const double* Lsc /* L = chol(Sigma
         S du[4], u[4], v[4];
         for (int i = 0; i < m; ++i) {                 // du = A_t L eps
             S acc = 0;
-            for (int j = 0; j < m; ++j) acc += Ft[i * m + j] * (S)e[j];
+            for (int j = 0; j < m; ++j) acc = mad<M>(Ft[i * m + j], (S)e[j], acc);
             du[i] = acc;
             u[i] = (S)U[t * m + i];
             v[i] = u[i] + du[i];                      // u_i + du_{i,k}
@@ -534,9 +561,9 @@ double rollout_one(const oracle_problem* pb, const double* Lsc /* L = chol(Sigma
         S duGdu = 0, uRdu = 0, uRu = 0;
         for (int i = 0; i < m; ++i)
             for (int j = 0; j < m; ++j) {
-                duGdu += du[i] * Gt[i * m + j] * du[j];
-                uRdu += u[i] * Rt[i * m + j] * du[j];
-                uRu += u[i] * Rt[i * m + j] * u[j];
+                duGdu = mad<M>(du[i] * Gt[i * m + j], du[j], duGdu);
+                uRdu = mad<M>(u[i] * Rt[i * m + j], du[j], uRdu);
+                uRu = mad<M>(u[i] * Rt[i * m + j], u[j], uRu);
             }
         // q~ = q + 1/2 du'Gamma~^{-1} du + u'R du + 1/2 u'R u
         S qt = q + (S)0.5 * duGdu + uRdu + (S)0.5 * uRu;
@@ -814,14 +841,15 @@ void oracle_shift(double* U, int32_t T, int32_t m, const double* u_init) {
     for (int i = 0; i < m; ++i) U[(T - 1) * m + i] = u_init[i];
 }
 
-// Crash-decision margin of each sample (conditioning filter, reading A19'): the fp64
-// rollout of sample k; at every step up to and including the first crash (C = 1
-// once the vehicle touches the ground or a cylinder), the distance of the decision from its
-// threshold, min(|z - ground_z|, |surface distance to the nearest cylinder|).  A sample whose
+// Decision margins of each sample (conditioning filter): the fp64 rollout of sample k; at every
+// step up to and including the first crash (C = 1 once the vehicle touches the
+// ground or a cylinder), the distance of a decision from its threshold.  mode 0 (crash, DESIGN.md
+// reading A19'): min(|z - ground_z|, |surface distance to the nearest cylinder|) -- a sample whose
 // margin is below the fp32 trajectory error can legitimately crash one step earlier or later in
-// an fp32 rollout.  Plants other than the quadrotor: +inf.  Returns 0 ok.
-int oracle_crash_margin(const oracle_problem* pb, const double* x0, const double* U,
-                        const float* eps, int64_t K, int32_t nthreads, double* margin) {
+// an fp32 rollout; mode 1 (Euler guard, A19''): |cos phi|.  Plants other than the quadrotor:
+// +inf.  Returns 0 ok.
+static int decision_margin(const oracle_problem* pb, const double* x0, const double* U,
+                           const float* eps, int64_t K, int32_t nthreads, double* margin, int mode) {
     if (!problem_ok(pb) || K < 0) return 1;
     double L[16];
     if (!cholesky(pb->Sigma, pb->m, L)) return 2;
@@ -852,6 +880,7 @@ int oracle_crash_margin(const oracle_problem* pb, const double* x0, const double
                     const double dx = x[0] - pb->obstacles[2 * j], dy = x[1] - pb->obstacles[2 * j + 1];
                     mt = std::min(mt, std::fabs(std::sqrt(dx * dx + dy * dy) - pb->params[22]));
                 }
+                if (mode == 1) mt = std::fabs(std::cos(x[6]));   // Euler-guard margin (A19'')
                 if (!std::isfinite(mt)) mt = 0.0;          // a diverged state: no margin
                 mk = std::min(mk, mt);
             }
@@ -859,6 +888,22 @@ int oracle_crash_margin(const oracle_problem* pb, const double* x0, const double
         margin[k] = mk;
     }
     return 0;
+}
+
+int oracle_crash_margin(const oracle_problem* pb, const double* x0, const double* U,
+                        const float* eps, int64_t K, int32_t nthreads, double* margin) {
+    return decision_margin(pb, x0, U, eps, K, nthreads, margin, 0);
+}
+
+// Euler-guard margin of each sample (conditioning filter, reading A19''): the ZXY
+// Euler-angle rate psi' = (-sin th p + cos th r) / cos phi is singular at cos phi = 0 (gimbal
+// lock); reading A12 guards the divisor as sign(cos phi) max(|cos phi|, cphi_min), so inside the
+// band |cos phi| < cphi_min the rate is decided by the SIGN of cos phi (a discontinuity) and the
+// trajectory chatters across it.  Returns, per sample, min over the steps up to and including
+// the first crash of |cos phi_{t+1}| of the fp64 rollout (+inf for the other plants).
+int oracle_euler_margin(const oracle_problem* pb, const double* x0, const double* U,
+                        const float* eps, int64_t K, int32_t nthreads, double* margin) {
+    return decision_margin(pb, x0, U, eps, K, nthreads, margin, 1);
 }
 
 // States of one rollout (for plots/debugging): xs [T+1][n], with the sample's eps column.

@@ -100,6 +100,7 @@ def lib():
         L.oracle_rollout_stepcosts.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int32, dp, C.c_int32]
         L.oracle_update_ctg.argtypes = [pp, dp, fp, C.c_int64, dp, dp, dp]
         L.oracle_crash_margin.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int32, dp]
+        L.oracle_euler_margin.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int32, dp]
         L.oracle_trajectory.argtypes = [pp, dp, dp, fp, C.c_int64, C.c_int64, dp]
         _LIB = L
     return _LIB
@@ -285,14 +286,17 @@ def cost_to_go(stepcosts):
 
 
 def well_conditioned_ctg(pb: Problem, x0, U, eps, rel=1e-5, nthreads=0):
-    """SURVEY A19 applied to the cost-to-go: sample k is well-conditioned iff at every t both fp32
-    twins' S~_{t,k} are within rel * max(|S~_{0,k}|, 1) of fp64.  Returns (mask[K], ctg fp64 [T][K])."""
+    """SURVEY A19 applied to the cost-to-go: sample k is well-conditioned iff at every t the fp32
+    twins' S~_{t,k} (the three of `well_conditioned`) are within rel * max(|S~_{0,k}|, 1) of fp64
+    and its crash and Euler-guard margins pass (A19', A19'').  Returns (mask[K], ctg fp64 [T][K])."""
     ref = cost_to_go(rollout_stepcosts(pb, x0, U, eps, nthreads))
     scale = np.maximum(np.abs(ref[0]), 1.0)
     ok = np.ones(ref.shape[1], bool)
-    for mode in ("twin_f32", "twin_f32_via_f64"):
-        tw = cost_to_go(rollout_stepcosts(pb, x0, U, eps, nthreads, mode))
+    for mode, e in (("twin_f32", eps), ("twin_f32_via_f64", eps), ("twin_f32", perturb_ulp(eps))):
+        tw = cost_to_go(rollout_stepcosts(pb, x0, U, e, nthreads, mode))
         ok &= np.all(np.abs(tw - ref) <= rel * scale, axis=0)
+    ok &= crash_margin(pb, x0, U, eps, nthreads) >= CRASH_MARGIN
+    ok &= euler_margin(pb, x0, U, eps, nthreads) >= EULER_MARGIN
     return ok, ref
 
 
@@ -337,22 +341,54 @@ def crash_margin(pb: Problem, x0, U, eps, nthreads=0):
     return out
 
 
+def euler_margin(pb: Problem, x0, U, eps, nthreads=0):
+    """Per-sample min |cos phi| of the fp64 rollout over the steps up to the first crash
+    (quadrotor; +inf otherwise): the distance of the ZXY Euler-rate guard from its sign decision
+    (reading A19'')."""
+    x0 = np.ascontiguousarray(np.asarray(x0, np.float64))
+    U = np.ascontiguousarray(np.asarray(U, np.float64).reshape(pb.T, pb.m))
+    eps = np.ascontiguousarray(np.asarray(eps, np.float32))
+    out = np.zeros(eps.shape[1])
+    assert lib().oracle_euler_margin(pb.ptr(), _dp(x0), _dp(U), _fp(eps), eps.shape[1], nthreads, _dp(out)) == 0
+    return out
+
+
 CRASH_MARGIN = 1e-4     # m; DESIGN.md reading A19' (>= 10x the fp32 position error at 50 m)
+EULER_MARGIN = 1e-4     # |cos phi|; DESIGN.md reading A19'' (the guard's sign decision)
+
+
+def perturb_ulp(eps):
+    """eps with every element moved by exactly one ulp, up or down by a fixed hash of its own bits
+    (deterministic, independent of how the columns are chunked): the input of the third
+    conditioning twin (reading A19, round 2) -- a rollout whose cost moves by more than
+    the twin tolerance under last-bit changes of its inputs is not rolled out stably in fp32."""
+    e = np.ascontiguousarray(np.asarray(eps, np.float32))
+    b = e.view(np.uint32).astype(np.uint64)
+    up = ((b * np.uint64(0x9E3779B1)) >> np.uint64(31)) & np.uint64(1)
+    return np.nextafter(e, np.where(up == 1, np.float32(np.inf), np.float32(-np.inf))).astype(np.float32)
 
 
 def well_conditioned(pb: Problem, x0, U, eps, ref_costs=None, rel=1e-5, nthreads=0,
-                     crash_tol=CRASH_MARGIN):
-    """sample k is well-conditioned iff both fp32 twins are within
-    rel * max(|S_k|, 1) of the fp64 cost, and (reading A19') no crash decision of its fp64
-    rollout lies within crash_tol of its threshold.  Returns (mask, ref_costs)."""
+                     crash_tol=CRASH_MARGIN, euler_tol=EULER_MARGIN, perturbed=True):
+    """sample k is well-conditioned iff the fp32 twins are within rel * max(|S_k|, 1)
+    of the fp64 cost -- twin 1 (libm fp32), twin 2 (fma updates, fp64 transcendentals) and
+    (round 2) twin 1 on the one-ulp-perturbed noise `perturb_ulp(eps)` -- and no decision of its
+    fp64 rollout lies within the fp32 resolution of its threshold: crash (reading A19', crash_tol
+    m) and the sign of the Euler-rate guard (reading A19'', |cos phi| >= euler_tol).
+    Returns (mask, ref_costs)."""
     if ref_costs is None:
         ref_costs = rollout_costs(pb, x0, U, eps, "fp64", nthreads)
-    a = rollout_costs(pb, x0, U, eps, "twin_f32", nthreads)
-    b = rollout_costs(pb, x0, U, eps, "twin_f32_via_f64", nthreads)
     scale = np.maximum(np.abs(ref_costs), 1.0)
-    mask = (np.abs(a - ref_costs) <= rel * scale) & (np.abs(b - ref_costs) <= rel * scale)
+    mask = np.ones(len(ref_costs), bool)
+    twins = [("twin_f32", eps), ("twin_f32_via_f64", eps)]
+    if perturbed:
+        twins.append(("twin_f32", perturb_ulp(eps)))
+    for mode, e in twins:
+        mask &= np.abs(rollout_costs(pb, x0, U, e, mode, nthreads) - ref_costs) <= rel * scale
     if crash_tol:
         mask &= crash_margin(pb, x0, U, eps, nthreads) >= crash_tol
+    if euler_tol:
+        mask &= euler_margin(pb, x0, U, eps, nthreads) >= euler_tol
     return mask, ref_costs
 
 

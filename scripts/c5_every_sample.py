@@ -1,0 +1,109 @@
+"""Every sample of C5 (quadrotor, K = 2^22, T = 200, 50 cylinders) against the fp64 oracle, in the
+launch configuration bench.py times (the default packed fused-noise kernel, one CUDA-graph step).
+
+  * noise: the device stream (mppi_noise) of all 2^22 x 200 x 4 normals bitwise against
+    oracle.noise, chunk by chunk;
+  * costs: every sample's S~ from the C5 kernel against the oracle's fp64 rollout, within 1e-4
+    relative on the well-conditioned samples (reading A19/A19'), the excluded count reported;
+  * k*: the GPU's argmin against the oracle's where the fp64 gap exceeds the measured error.
+
+Evidence run, not part of the pytest suite (about 10-20 minutes of host time on the GPU box):
+    python scripts/c5_every_sample.py [--chunk 65536] [--out gpurun_out/c5_every_sample.txt]
+"""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from mppi_inputs import get  # noqa: E402
+from paper_1509_01149_b200 import from_workload  # noqa: E402
+
+COST_RTOL = 1e-4
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--chunk", type=int, default=65536)
+    ap.add_argument("--out", default="gpurun_out/c5_every_sample.txt")
+    ap.add_argument("--limit", type=int, default=0, help="only the first N chunks (smoke)")
+    a = ap.parse_args()
+    import oracle.oracle as oracle   # test infrastructure (the checker), loaded by this script only
+
+    w = get("C5")
+    K, T, m = w.K, w.T, w.m
+    g = from_workload(w)
+    U = torch.tensor(w.U0, device="cuda")
+    costs, key = g.rollout_costs(w.x0, U, w.seed, 0)
+    kern = g.last_kernels()
+    assert any("rollout_kernel_x2" in n for n in kern), kern
+    c_gpu = costs.cpu().numpy().astype(np.float64)
+    eps_dev = g.noise(w.seed, 0)
+    torch.cuda.synchronize()
+    pb = oracle.Problem(w.plant, T=T, dt=w.dt, lam=w.lam, nu=w.nu, Sigma=w.Sigma, R=w.R,
+                        obstacles=w.obstacles)
+    n_chunks = (K + a.chunk - 1) // a.chunk
+    if a.limit:
+        n_chunks = min(n_chunks, a.limit)
+    ref_all = np.full(K, np.nan)
+    ok_all = np.zeros(K, bool)
+    noise_mismatch = 0
+    worst = (0.0, -1)
+    t0 = time.time()
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    log = open(a.out, "w")
+
+    def say(s):
+        print(s, flush=True)
+        log.write(s + "\n")
+        log.flush()
+
+    say("# C5 every sample: kernel %s, K=%d T=%d m=%d, seed %d, step 0; chunk %d"
+        % (kern, K, T, m, w.seed, a.chunk))
+    for ci in range(n_chunks):
+        k0 = ci * a.chunk
+        n = min(a.chunk, K - k0)
+        ref_eps = oracle.noise(w.seed, 0, T, n, m, k0=k0)
+        got = eps_dev[:, k0:k0 + n, :].cpu().numpy()
+        noise_mismatch += int(np.count_nonzero(got.view(np.uint32) != ref_eps.view(np.uint32)))
+        del got
+        ok, ref = oracle.well_conditioned(pb, w.x0, w.U0, ref_eps)
+        ref_all[k0:k0 + n] = ref
+        ok_all[k0:k0 + n] = ok
+        err = np.abs(c_gpu[k0:k0 + n] - ref) / np.maximum(np.abs(ref), 1.0)
+        if ok.any():
+            j = int(np.argmax(np.where(ok, err, -1.0)))
+            if err[j] > worst[0]:
+                worst = (float(err[j]), k0 + j)
+        badk = np.nonzero(ok & (err > COST_RTOL))[0]
+        bad = int(badk.size)
+        for j in badk:
+            say("  over 1e-4: k=%d gpu %.9g fp64 %.9g rel err %.3g" % (k0 + j, c_gpu[k0 + j], ref[j], err[j]))
+        say("chunk %3d k0 %8d: noise mismatches %d, excluded %d, over 1e-4 on kept %d, max rel err kept %.3g"
+            " (%.0f s)" % (ci, k0, noise_mismatch, int((~ok).sum()), bad,
+                           float(err[ok].max()) if ok.any() else 0.0, time.time() - t0))
+    done = n_chunks * a.chunk if n_chunks * a.chunk < K else K
+    ok = ok_all[:done]
+    err = np.abs(c_gpu[:done] - ref_all[:done]) / np.maximum(np.abs(ref_all[:done]), 1.0)
+    n_bad = int(np.count_nonzero(ok & (err > COST_RTOL)))
+    say("SUMMARY samples %d: noise %d normals, %d bit mismatches; well-conditioned %d (excluded %d = %.5f);"
+        " costs over 1e-4 relative on kept: %d; max rel err on kept %.3g at k=%d; overall max %.3g"
+        % (done, done * T * m, noise_mismatch, int(ok.sum()), int((~ok).sum()), 1 - ok.mean(), n_bad,
+           worst[0], worst[1], float(np.nanmax(err))))
+    if done == K:
+        kk = int(key.item()) & 0xFFFFFFFF
+        kr = int(np.argmin(ref_all))
+        order = np.sort(ref_all)
+        gap = order[1] - order[0]
+        say("k*: GPU %d (S %.9g), oracle %d (S %.9g), fp64 gap to the runner-up %.3g, GPU argmin of its own"
+            " costs %d" % (kk, c_gpu[kk], kr, ref_all[kr], gap, int(np.argmin(c_gpu))))
+    log.close()
+    return 0 if (noise_mismatch == 0 and n_bad == 0 and (1 - ok.mean()) <= 0.01) else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -259,3 +259,58 @@ def test_linear_plant(oracle):
     x1, q, _ = oracle.plant_step(pb, x, [2.0])
     assert np.allclose(x1, x + 0.1 * (A @ x + B @ [2.0]))
     assert q == pytest.approx(x1 @ Q @ x1)
+
+
+def test_quad_euler_margin_closed_form(oracle):
+    """Reading A19'' filter: a constant roll rate p with equal thrusts and theta = r = 0 keeps every
+    other rate zero, so explicit Euler gives phi_t = t p dt exactly up to rounding and the margin is
+    min_{t=1..T} |cos(t p dt)| (no crash: z0 high, thrust at hover).  Choosing p dt = (pi/2)/k
+    puts step k on the singularity (margin ~ 0)."""
+    T, dt = 40, 0.02
+    pb = P(oracle, "quadrotor", T=T, obstacles=[[40.0, 0.0]])
+    U = np.full((T, 4), HOVER)
+    eps = np.zeros((T, 1, 4), np.float32)
+    for prate in (3.1, 5.0, -7.3):
+        x0 = quad_state(pos=(0, 0, 50.0), rates=(prate, 0, 0))
+        t = np.arange(1, T + 1)
+        want = float(np.min(np.abs(np.cos(t * prate * dt))))
+        assert oracle.euler_margin(pb, x0, U, eps)[0] == pytest.approx(want, rel=1e-9, abs=1e-14)
+    x0 = quad_state(pos=(0, 0, 50.0), rates=(math.pi / 2 / (7 * dt), 0, 0))
+    assert oracle.euler_margin(pb, x0, U, eps)[0] < 1e-12
+    pc = P(oracle, "cartpole", T=5)
+    assert np.isinf(oracle.euler_margin(pc, [0, 0, 0, 0], np.zeros((5, 1)), np.zeros((5, 1, 1), np.float32))[0])
+
+
+def test_perturb_ulp_moves_every_element_by_one_ulp(oracle):
+    """The third conditioning twin's input: every element exactly one ulp away (up or down), a
+    fixed function of the element's own bits (so chunking the columns does not change it), both
+    directions used."""
+    e = oracle.noise(3, 0, 7, 301, 4)
+    p = oracle.perturb_ulp(e)
+    assert p.dtype == np.float32 and p.shape == e.shape
+    up = np.nextafter(e, np.float32(np.inf))
+    dn = np.nextafter(e, np.float32(-np.inf))
+    assert np.all((p == up) | (p == dn)) and np.all(p != e)
+    frac_up = np.mean(p == up)
+    assert 0.4 < frac_up < 0.6
+    assert np.array_equal(oracle.perturb_ulp(e[:, 100:200]), p[:, 100:200])
+
+
+def test_twin2_uses_fused_updates_and_twins_stay_close(oracle):
+    """twin 2 runs the Euler and cost updates with fmaf, so its rounding sequence
+    differs from twin 1's (not bitwise equal on a tumbling quadrotor batch) while both stay
+    within the fp32 resolution of fp64 on well-behaved samples; the fp64 reference is unchanged by
+    the twins' code (its pins elsewhere stay exact)."""
+    T = 60
+    pb = P(oracle, "quadrotor", T=T, nu=50.0, obstacles=[[3.0, 0.5], [-2.0, 4.0]])
+    x0 = quad_state()
+    U = np.full((T, 4), HOVER)
+    eps = oracle.noise(11, 0, T, 512, 4)
+    ref = oracle.rollout_costs(pb, x0, U, eps)
+    a = oracle.rollout_costs(pb, x0, U, eps, "twin_f32")
+    b = oracle.rollout_costs(pb, x0, U, eps, "twin_f32_via_f64")
+    assert not np.array_equal(a, b)
+    ok = oracle.well_conditioned(pb, x0, U, eps, ref_costs=ref)[0]
+    assert ok.mean() > 0.9
+    rel = np.abs(np.stack([a, b]) - ref) / np.maximum(np.abs(ref), 1.0)
+    assert rel[:, ok].max() <= 1e-5
