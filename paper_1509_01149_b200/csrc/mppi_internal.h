@@ -19,7 +19,11 @@ constexpr int kRolloutThreads = 128;
 constexpr size_t kRolloutStaticSmem = 2304;
 constexpr int kWsumThreads = 256;
 #ifndef MPPI_X2_MINB
-#define MPPI_X2_MINB 4
+// packed rollout: 3 resident CTAs per SM (register cap 168; 155 used, no spills).  Measured
+// against 4 CTAs / 128 registers: -0.25 % at K = 2^22 ... -2.6 % at 2^16, 5 CTAs (96 registers,
+// spills) +3.5 %, 2 CTAs +6.5 % (profiles/r2_ab_occupancy.txt): the step loop is bound by the
+// FMA-heavy pipe and issue, not by the number of warps hiding latency
+#define MPPI_X2_MINB 3
 #endif
 #ifndef MPPI_EPI_ROWS
 #define MPPI_EPI_ROWS 2      // fused-reduction epilogue: noise rows per warp pass (8 float4 loads each)
