@@ -106,7 +106,7 @@ bool all_finite(const float* p, int n) {
 // Every centre that can be the fp32 minimum for a point the kernel assigns to the cell is
 // therefore listed (slack >> the cell-assignment rounding, margin >> the fp32 error of d^2 over
 // the cell), and the minimum over the list equals the minimum over all centres bit for bit.
-// Border cells also cover a band of 100 spacings outside the grid (their rectangles are grown
+// Border cells also cover a band of 30 spacings outside the grid (their rectangles are grown
 // outward; an affine difference still peaks at a corner).  Cells with more than kCellMaxCand
 // candidates, and points beyond the band, take the full loop.
 void build_cell_grid(Ctx& c, const float* xy, int n) {
@@ -137,7 +137,13 @@ void build_cell_grid(Ctx& c, const float* xy, int n) {
     const int nx = (int)ceil(W / h), ny = (int)ceil(H / h);
     const double gx0 = (float)(xmin - pad), gy0 = (float)(ymin - pad);   // representable origin
     // the kernel's fp32 cell assignment floor(fma(p, 1/h, -g0/h)) is off by < 1e-4 cells
-    const double band = ceil(100.0 * spacing / h);             // cells; beyond it: full search
+    // cells; beyond it: full search (replay).  30 spacings: a border cell's strip is short enough
+    // that no cell of the configs' forests needs more than kCellMaxCand candidates (at 100
+    // spacings six top-border strips overflowed, and once U has converged -- trajectories
+    // reaching 8-20 m past the forest -- 6 % of the packed rollout's warps replayed a pair:
+    // C4 241 -> 435 us per step; profiles/r2_grid_band.txt), while sampled quadrotors stay far
+    // inside it (<= 20 m past the grid in 8192 fp64 rollouts)
+    const double band = ceil(30.0 * spacing / h);
     const double slack = 1e-3 * h + 1e-6 * (fabs(gx0) + fabs(gy0) + W + H + 2 * band * h);
     std::vector<uint32_t> words((size_t)nx * ny);
     std::vector<double> d2(4 * (size_t)n);
