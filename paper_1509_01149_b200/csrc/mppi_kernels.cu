@@ -2199,7 +2199,10 @@ cudaError_t launch_epi_combine(Ctx& c, const long long* key) {
 bool fused_noise_applies(const Ctx& c) {
     // GEN kernels only once the step is throughput-bound (measured: -2..4 % at K = 2^20 for the
     // one-sample kernel; at small K the per-thread noise lengthens the latency-bound step loop)
-    if (!c.fuse_noise || c.K_loc < kPackedMinK) return false;
+#ifndef MPPI_GEN_MIN_K
+#define MPPI_GEN_MIN_K kPackedMinK
+#endif
+    if (!c.fuse_noise || c.K_loc < MPPI_GEN_MIN_K) return false;
     if (c.plant == MPPI_PLANT_QUADROTOR) {
         if (c.diag && !c.per_t && c.pack2) return true;   // packed kernel (any obstacle path)
         return grid_on(c);                                 // one-sample grid kernel (any Sigma, A_t)
