@@ -507,6 +507,15 @@ mppi_status_t mppi_obstacle_grid(const float* xy, int32_t n, uint32_t* words, in
  * and eta (eta is this rank's local sum unless mppi_apply ran with a summed buffer). */
 mppi_status_t mppi_get_stats(mppi_ctx* ctx, mppi_stats_t* out /* HOST */);
 
+/* mppi_replay_count — SYNCHRONOUS: waits for the stream, then returns in *out (HOST) the number
+ * of rollouts this context has re-run since creation (cumulative, one per sample on the
+ * one-sample kernels, one per sample pair on the packed quadrotor kernel).  A rollout is re-run
+ * from x0 after its step loop, with the per-step accurate fallbacks, when an angle left the fast
+ * sin/cos range or a position left the obstacle grid's band or met an overflowing cell (DESIGN.md
+ * §6); results are identical either way, only the time differs.  Telemetry for that slow path.
+ * Errors: INVALID_ARG (NULL out), CUDA. */
+mppi_status_t mppi_replay_count(mppi_ctx* ctx, int64_t* out);
+
 /* Number of kernels the last mppi_optimize / split-phase call enqueued (for launch accounting). */
 int32_t mppi_last_launch_count(const mppi_ctx* ctx);
 

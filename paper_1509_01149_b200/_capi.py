@@ -106,7 +106,7 @@ EXPORTS = ["mppi_create", "mppi_destroy", "mppi_info", "mppi_set_stream", "mppi_
            "mppi_optimize_host", "mppi_rollout_costs", "mppi_accumulate", "mppi_gather_record_len", "mppi_accumulate_record", "mppi_apply_gathered", "mppi_apply",
            "mppi_shift", "mppi_noise", "mppi_feynman_kac", "mppi_closed_loop", "mppi_set_weighting",
            "mppi_cost_to_go", "mppi_set_sampling_transform", "mppi_nccl_unique_id", "mppi_nccl_attach",
-           "mppi_obstacle_grid", "mppi_plant_step", "mppi_get_stats",
+           "mppi_obstacle_grid", "mppi_plant_step", "mppi_get_stats", "mppi_replay_count",
            "mppi_last_launch_count", "mppi_last_kernels", "mppi_profile_enable", "mppi_profile_read", "mppi_last_error", "mppi_status_string", "mppi_abi_version"]
 
 _lib = None
@@ -179,6 +179,8 @@ def lib():
     L.mppi_plant_step.restype = st
     L.mppi_get_stats.argtypes = [vp, C.POINTER(stats_t)]
     L.mppi_get_stats.restype = st
+    L.mppi_replay_count.argtypes = [vp, C.POINTER(C.c_int64)]
+    L.mppi_replay_count.restype = st
     L.mppi_last_launch_count.argtypes = [vp]
     L.mppi_last_launch_count.restype = C.c_int32
     L.mppi_last_kernels.argtypes = [vp, C.c_char_p, C.c_int64]

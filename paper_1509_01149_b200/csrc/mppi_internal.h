@@ -83,6 +83,7 @@ struct DeviceStats {
     long long min_key;
     float eta;
     int plant_crashed;   // crash flag of the device-resident plant (mppi_closed_loop)
+    unsigned long long replays;   // cumulative: rollouts re-run after the loop (mppi_replay_count)
 };
 
 struct Ctx {

@@ -156,6 +156,7 @@ struct RolloutArgs {
     float* costs;           // [K_loc] (context copy)
     float* costs_out;       // [K_loc] caller copy or nullptr
     long long* min_key;     // reset to INT64_MAX before launch
+    unsigned long long* replays;   // cumulative count of replayed rollouts (one per sample / pair)
     const float4* obs;      // negated obstacle pairs
     int n_obs_pairs;
     int T;
@@ -446,7 +447,10 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
         } else {
             eps_ring_loop<M>(a.eps, row, a.T, k, sRing, [&](int t, const float* e) { ro.step(rec++, e, t == 0, t); });
         }
-        if (__builtin_expect(ro.slow, 0)) ro.replay(GEN ? a.eps_out : a.eps, sRec);
+        if (__builtin_expect(ro.slow, 0)) {
+            atomicAdd(a.replays, 1ull);
+            ro.replay(GEN ? a.eps_out : a.eps, sRec);
+        }
         const float S = ro.finish();
         a.costs[k] = S;
         if (a.costs_out) a.costs_out[k] = S;
@@ -659,6 +663,7 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
             cur = slot_sum - cur;
         }
         if (__builtin_expect(!(amax <= kSinCosFastMax) || st.miss, 0)) {
+            atomicAdd(a.replays, 1ull);   // one per replayed pair
             // An angle left the fast sin/cos range, or a position left the obstacle grid's band
             // (or hit an overflow cell), somewhere on this pair's trajectories: replay both from
             // x0 with the per-step accurate fallbacks (the inline-fallback semantics), reading
@@ -1993,6 +1998,7 @@ static void fill_rollout_args(Ctx& c, const typename Plant::Params& P, const flo
     a.costs = c.d_costs;
     a.costs_out = costs_out;
     a.min_key = &c.d_stats->min_key;
+    a.replays = &c.d_stats->replays;
     a.obs = c.d_obs;
     a.n_obs_pairs = c.n_obs_pairs;
     a.T = c.T;

@@ -569,6 +569,7 @@ mppi_status_t mppi_create(const mppi_dynamics_t* dynamics, const mppi_cost_t* co
     st0.min_key = LLONG_MAX;
     st0.eta = 0.0f;
     st0.plant_crashed = 0;
+    st0.replays = 0;
     if ((e = cudaMemcpy(c.d_key_init, &kinit, sizeof(kinit), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMemcpy(c.d_stats, &st0, sizeof(st0), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (c.n_obs_pairs > 0 &&
@@ -1113,6 +1114,17 @@ mppi_status_t mppi_get_stats(mppi_ctx* ctx, mppi_stats_t* out) {
     out->k_star = (int64_t)(uint32_t)(h.min_key & 0xffffffffLL);
     out->s_min = smin;
     out->eta = h.eta;
+    return MPPI_OK;
+}
+
+mppi_status_t mppi_replay_count(mppi_ctx* ctx, int64_t* out) {
+    if (mppi_status_t s = check_ctx(ctx)) return s;
+    if (!out) return fail(MPPI_ERR_INVALID_ARG, "out is NULL");
+    Ctx& c = ctx->c;
+    MPPI_CUDA(cudaStreamSynchronize(c.stream), "stream sync");
+    unsigned long long n = 0;
+    MPPI_CUDA(cudaMemcpy(&n, &c.d_stats->replays, sizeof(n), cudaMemcpyDeviceToHost), "replay count D2H");
+    *out = (int64_t)n;
     return MPPI_OK;
 }
 

@@ -278,6 +278,13 @@ class MPPI:
         A.check(self.lib.mppi_get_stats(self.ctx, C.byref(out)))
         return dict(k_star=out.k_star, s_min=out.s_min, eta=out.eta)
 
+    def replay_count(self):
+        """mppi_replay_count: rollouts re-run after their step loop since creation (telemetry of
+        the slow path; results are identical either way)."""
+        out = C.c_int64()
+        A.check(self.lib.mppi_replay_count(self.ctx, C.byref(out)))
+        return out.value
+
     def profile_enable(self, enable=True):
         A.check(self.lib.mppi_profile_enable(self.ctx, 1 if enable else 0))
 
