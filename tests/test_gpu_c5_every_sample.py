@@ -8,7 +8,7 @@ bench times (the packed two-sample kernel drawing its own noise):
     keeps (readings A19, A19', A19''), at most 1 % excluded;
   * k* equal to the oracle's argmin (the fp64 gap to the runner-up is far above the error).
 
-About 4 minutes on a 16-core GPU host (the oracle's rollouts; scripts/c5_every_sample.py writes
+About 4 minutes on a 16-core GPU host (the oracle's rollouts; tests/tools/c5_every_sample.py writes
 the same comparison as a per-chunk report, profiles/r2_c5_every_sample.txt)."""
 import numpy as np
 import pytest

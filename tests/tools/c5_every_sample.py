@@ -8,15 +8,16 @@ launch configuration bench.py times (the default packed fused-noise kernel, one 
   * k*: the GPU's argmin against the oracle's where the fp64 gap exceeds the measured error.
 
 Evidence run, not part of the pytest suite (about 10-20 minutes of host time on the GPU box):
-    python scripts/c5_every_sample.py [--chunk 65536] [--out gpurun_out/c5_every_sample.txt]
+    python tests/tools/c5_every_sample.py [--chunk 65536] [--out gpurun_out/c5_every_sample.txt]
 """
 import argparse
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 

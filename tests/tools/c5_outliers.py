@@ -5,13 +5,14 @@ the C5 kernel's costs), find the offending samples, and compare the per-step cos
 (cost-to-go mode, differenced) with the fp64 oracle and both twins to locate the first divergent
 step; print the fp64 state around it.
 
-    python scripts/c5_outliers.py 8 17 48 51 53 59
+    python tests/tools/c5_outliers.py 8 17 48 51 53 59
 """
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 

@@ -1,12 +1,13 @@
 """Per-step cost profile of chosen C5 samples: GPU (packed kernel, cost-to-go mode, differenced)
 against the fp64 oracle and both fp32 twins; prints |q_gpu - q64| and |q_twin - q64| per step with
 the fp64 |cos phi| (distance from the ZXY Euler singularity).
-    python scripts/c5_profile_samples.py 1168267 575396"""
+    python tests/tools/c5_profile_samples.py 1168267 575396"""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
