@@ -316,7 +316,7 @@ typedef enum {
                                           bit-identical to the separate pass, and the per-t CTA
                                           minima) and the per-(CTA, t) weighted sums in their
                                           epilogue, rescaled to S_min,t afterwards (default 1) */
-    MPPI_OPTION_GATHER_COMBINE = 9     /* sharded step with the library's communicator, trajectory
+    MPPI_OPTION_GATHER_COMBINE = 9,    /* sharded step with the library's communicator, trajectory
                                           weights: ONE collective instead of two -- every rank forms
                                           its weighted sums against its own minimum, an ncclAllGather
                                           exchanges the [key, eta_r, A_r] records, and every rank
@@ -324,6 +324,22 @@ typedef enum {
                                           (PAPER.md:320 is invariant to the shift).  k* and S_min
                                           identical, U equal to rounding (single rank: bitwise)
                                           (default 1) */
+    MPPI_OPTION_NOISE_AHEAD = 10       /* K_loc < 65536 (the noise is its own pass), CUDA-graph
+                                          path, one GPU: after the step's graph, the noise of
+                                          (seed, step + 1) is drawn into a second buffer on a
+                                          library-owned side stream, and a following call with
+                                          exactly that (seed, step) skips its noise kernel (it
+                                          waits on the side stream's event instead) -- the noise
+                                          leaves the control update's critical path (U is
+                                          complete on the context stream without it).  Noise is
+                                          a pure function of (seed, step, k), so results are
+                                          bitwise identical; any other call that rewrites the
+                                          context's noise buffer discards the drawn-ahead noise.
+                                          Default 0: a synchronous control loop at C3 (race car,
+                                          K = 16384, T = 150) gains 8 us of its 67 us p50, but
+                                          back-to-back steps lose 5 us and C1/C2 gain nothing
+                                          (+9 us of host enqueue for the side launch;
+                                          profiles/r2_ab_noise_ahead_latency.txt) */
 } mppi_option_t;
 
 /* mppi_set_option — execution options that never change results (FUSED_REDUCTION: U to rounding). */

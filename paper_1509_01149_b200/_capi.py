@@ -23,6 +23,7 @@ MPPI_OPTION_PDL = 6
 MPPI_OPTION_SPARSE_REDUCTION = 7
 MPPI_OPTION_FUSED_REDUCTION = 8
 MPPI_OPTION_GATHER_COMBINE = 9
+MPPI_OPTION_NOISE_AHEAD = 10
 MPPI_WEIGHTS_TRAJECTORY, MPPI_WEIGHTS_COST_TO_GO = 0, 1
 
 

@@ -161,7 +161,20 @@ struct Ctx {
     bool collect = false;                 // launchers append to `pending` instead of launching
     bool x0_on_device = false;            // launch_rollout's x0 is a device pointer (closed loop)
     std::vector<KLaunch> pending;
-    GraphState graphs[2];
+    // CUDA-graph replay: [0] generated noise, [1] supplied noise, [2] noise drawn ahead (this
+    // step's noise came from the previous call's side branch)
+    GraphState graphs[3];
+    // noise ahead (MPPI_OPTION_NOISE_AHEAD): after a separate-noise step's graph, the NEXT
+    // step's noise (seed, step + 1) is drawn on a side stream into the other of two buffers; the
+    // next call with that (seed, step) skips its noise kernel (and waits for ev_side_done)
+    bool noise_ahead = false;             // default 0 (profiles/r2_ab_noise_ahead_latency.txt)
+    float* d_eps2 = nullptr;              // [T][K_loc][m] (K_loc < kPackedMinK only)
+    cudaStream_t side_stream = nullptr;
+    cudaEvent_t ev_chain_done = nullptr, ev_side_done = nullptr;
+    bool side_pending = false;            // a side launch may still be running
+    bool ahead_ok = false;
+    const float* ahead_buf = nullptr;
+    uint64_t ahead_seed = 0, ahead_step = 0;
     GraphState loop_graph;                // mppi_closed_loop's n-step graph, reused while its kernel sequence is unchanged
     // row (e): a communicator the library drives itself (mppi_nccl_attach)
     void* nccl = nullptr;                 // ncclComm_t

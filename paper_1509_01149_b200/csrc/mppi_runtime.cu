@@ -329,6 +329,7 @@ void free_graphs(Ctx& c) {
 }
 
 void free_ctx(Ctx& c) {
+    if (c.side_stream) cudaStreamSynchronize(c.side_stream);   // a noise drawn ahead may still write
     free_graphs(c);
     nccl_detach(c);
     cudaFree(c.d_commbuf);
@@ -344,6 +345,12 @@ void free_ctx(Ctx& c) {
     cudaFree(c.d_flags);
     cudaFree(c.d_epi);
     cudaFree(c.d_eps);
+    cudaFree(c.d_eps2);
+    if (c.ev_chain_done) cudaEventDestroy(c.ev_chain_done);
+    if (c.ev_side_done) cudaEventDestroy(c.ev_side_done);
+    if (c.side_stream) cudaStreamDestroy(c.side_stream);
+    c.side_stream = nullptr;
+    c.ev_chain_done = c.ev_side_done = nullptr;
     cudaFree(c.d_costs);
     cudaFree(c.d_key_init);
     cudaFree(c.d_part);
@@ -396,6 +403,11 @@ mppi_status_t do_rollout(Ctx& c, const float* x0, const float* U, uint64_t seed,
     if (!c.x0_on_device && !all_finite(x0, c.n)) return fail(MPPI_ERR_INVALID_ARG, "x0 must be finite");
     mppi_status_t s = sticky_check(c);
     if (s) return s;
+    c.ahead_ok = false;   // d_eps is rewritten below: a noise drawn ahead may be clobbered
+    if (c.side_pending) {   // ... and must not still be writing it
+        MPPI_CUDA(cudaStreamWaitEvent(c.stream, c.ev_side_done, 0), "wait for the noise drawn ahead");
+        c.side_pending = false;
+    }
     const float* eps = noise;
     const bool fused = !noise && fused_noise_applies(c);
     if (!noise && !fused) {
@@ -660,8 +672,13 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
     const float* eps = noise ? noise : c.d_eps;
     const bool fused = !noise && fused_noise_applies(c);
     c.epi_active = !noise && epi_applies(c);
+    // noise ahead: the separate-noise path draws (seed, step + 1) beside this step's chain
+    const bool ahead = !noise && !fused && c.noise_ahead && c.world == 1 && c.d_eps2 && c.side_stream;
+    const bool hit = ahead && c.ahead_ok && c.ahead_seed == seed && c.ahead_step == step;
+    if (hit) eps = c.ahead_buf;
+    float* next = ahead ? (eps == c.d_eps ? c.d_eps2 : c.d_eps) : nullptr;
     cudaError_t e = cudaSuccess;
-    if (!noise && !fused) e = launch_noise(c, seed, step, c.d_eps, true);
+    if (!noise && !fused && !hit) e = launch_noise(c, seed, step, c.d_eps, true);
     if (fused) {
         c.gen_eps = c.d_eps;
         c.gen_seed = seed;
@@ -673,7 +690,7 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
     c.epi_active = false;
     c.collect = false;
     if (e != cudaSuccess) return cuda_fail(e, "collecting the step's launches");
-    GraphState& G = c.graphs[noise ? 1 : 0];
+    GraphState& G = c.graphs[noise ? 1 : hit ? 2 : 0];
     bool same = G.exec && G.funcs.size() == c.pending.size();
     for (size_t i = 0; same && i < c.pending.size(); ++i) same = G.funcs[i] == c.pending[i].func;
     if (!same) {
@@ -682,12 +699,13 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
         G = GraphState();
         MPPI_CUDA(cudaGraphCreate(&G.graph, 0), "cudaGraphCreate");
         cudaGraphNode_t prev = nullptr;
-        if (noise || fused) {   // no K1 in the graph: the min key is reset by a copy node
+        if (noise || fused || hit) {   // no K1 on the chain: the min key is reset by a copy node
             MPPI_CUDA(cudaGraphAddMemcpyNode1D(&prev, G.graph, nullptr, 0, &c.d_stats->min_key, c.d_key_init,
                                                sizeof(long long), cudaMemcpyDeviceToDevice), "memcpy node");
         }
         bool prev_is_kernel = false;
-        for (KLaunch& L : c.pending) {
+        for (size_t li = 0; li < c.pending.size(); ++li) {
+            KLaunch& L = c.pending[li];
             cudaKernelNodeParams p = node_params(L);
             cudaGraphNode_t node;
             MPPI_CUDA(cudaGraphAddKernelNode(&node, G.graph, nullptr, 0, &p), "cudaGraphAddKernelNode");
@@ -722,8 +740,33 @@ static mppi_status_t optimize_graph(Ctx& c, const float* x0, float* U, uint64_t 
             G.last[i] = L;
         }
     }
+    // the noise drawn ahead by the previous call (side stream) must be complete before this
+    // step reads it -- or, on a miss, before this step rewrites a buffer it may still be writing
+    if (c.side_pending) {
+        MPPI_CUDA(cudaStreamWaitEvent(c.stream, c.ev_side_done, 0), "wait for the noise drawn ahead");
+        c.side_pending = false;
+    }
     MPPI_CUDA(cudaGraphLaunch(G.exec, c.stream), "cudaGraphLaunch");
     c.last_eps = eps;
+    c.ahead_ok = false;
+    if (ahead) {
+        // draw (seed, step + 1) on the side stream once this step's chain is done (its buffer was
+        // read by the previous step, which precedes this chain on the context stream): the update
+        // U is complete without waiting for it, and the next call waits for ev_side_done
+        MPPI_CUDA(cudaEventRecord(c.ev_chain_done, c.stream), "event record");
+        MPPI_CUDA(cudaStreamWaitEvent(c.side_stream, c.ev_chain_done, 0), "side stream wait");
+        cudaStream_t main = c.stream;
+        c.stream = c.side_stream;
+        const cudaError_t en = launch_noise(c, seed, step + 1, next, false);
+        c.stream = main;
+        MPPI_CUDA(en, "noise_kernel launch (ahead)");
+        MPPI_CUDA(cudaEventRecord(c.ev_side_done, c.side_stream), "event record");
+        c.side_pending = true;
+        c.ahead_ok = true;
+        c.ahead_buf = next;
+        c.ahead_seed = seed;
+        c.ahead_step = step + 1;
+    }
     return MPPI_OK;
 }
 
@@ -744,6 +787,21 @@ mppi_status_t mppi_set_option(mppi_ctx* ctx, mppi_option_t option, int32_t value
         case MPPI_OPTION_SPARSE_REDUCTION: ctx->c.sparse_wsum = value != 0; return MPPI_OK;
         case MPPI_OPTION_FUSED_REDUCTION: ctx->c.epi = value != 0; return MPPI_OK;
         case MPPI_OPTION_GATHER_COMBINE: ctx->c.gather_combine = value != 0; return MPPI_OK;
+        case MPPI_OPTION_NOISE_AHEAD: {
+            Ctx& c = ctx->c;
+            c.ahead_ok = false;
+            c.noise_ahead = value != 0;
+            // below the in-kernel-noise threshold the noise is its own pass: a second buffer, a
+            // side stream and the two events that order it (allocated once, on first enable)
+            if (c.noise_ahead && c.K_loc < kPackedMinK && !c.d_eps2) {
+                if (mppi_status_t a = dalloc(c, &c.d_eps2, (size_t)c.T * c.K_loc * c.m, "noise (ahead)")) return a;
+                if (cudaStreamCreateWithFlags(&c.side_stream, cudaStreamNonBlocking) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&c.ev_chain_done, cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&c.ev_side_done, cudaEventDisableTiming) != cudaSuccess)
+                    return fail(MPPI_ERR_CUDA, "side stream / events for the noise drawn ahead");
+            }
+            return MPPI_OK;
+        }
         case MPPI_OPTION_PDL:
             MPPI_CUDA(cudaStreamSynchronize(ctx->c.stream), "stream sync");
             ctx->c.use_pdl = value != 0;
@@ -1151,6 +1209,11 @@ mppi_status_t mppi_closed_loop(mppi_ctx* ctx, float* x, float* U, uint64_t seed,
     NvtxRange nvtx_("mppi_closed_loop");
     if (mppi_status_t s = check_ctx(ctx)) return s;
     Ctx& c = ctx->c;
+    c.ahead_ok = false;   // the loop's graph rewrites the noise buffer
+    if (c.side_pending) {
+        MPPI_CUDA(cudaStreamWaitEvent(c.stream, c.ev_side_done, 0), "wait for the noise drawn ahead");
+        c.side_pending = false;
+    }
     if (c.world != 1 && !c.nccl)
         return fail(MPPI_ERR_UNSUPPORTED, "mppi_closed_loop with world > 1 needs mppi_nccl_attach");
     if (c.plant == MPPI_PLANT_LINEAR) return fail(MPPI_ERR_UNSUPPORTED, "mppi_closed_loop: linear test plant");
