@@ -6,7 +6,10 @@ bench times (the packed two-sample kernel drawing its own noise):
     (SURVEY Appendix B; PAPER.md:101);
   * every sample's cost S~_k within 1e-4 relative on the samples the oracle's conditioning filter
     keeps (readings A19, A19', A19''), at most 1 % excluded;
-  * k* equal to the oracle's argmin (the fp64 gap to the runner-up is far above the error).
+  * k* equal to the oracle's argmin (the fp64 gap to the runner-up is far above the error);
+  * the update U' of the bench's step (fused reduction) against the oracle's update computed from
+    the ORACLE's costs (coupled, A20): every sample whose fp64 weight exceeds 1e-30 goes to the
+    oracle's reduction with its oracle-drawn noise, within 1e-5.
 
 About 4 minutes on a 16-core GPU host (the oracle's rollouts; tests/tools/c5_every_sample.py writes
 the same comparison as a per-chunk report, profiles/r2_c5_every_sample.txt)."""
@@ -55,3 +58,15 @@ def test_every_sample_of_c5(oracle):
     assert kk == int(np.argmin(c))
     assert order[1] - order[0] > 2 * np.max(np.abs(c - ref)[ok])
     assert kk == int(np.argmin(ref))
+    # coupled update: the oracle's weights from its own fp64 costs (S_min's sample is among the
+    # kept ones, so the dropped weights change eta and A by < K 1e-30 relative)
+    keep = np.nonzero(np.exp(-(ref - ref.min()) / w.lam) > 1e-30)[0]
+    eps_keep = np.concatenate([oracle.noise(w.seed, 0, T, 1, m, k0=int(k)) for k in keep], axis=1)
+    Uo, kstar, _, _, _ = oracle.update(pb, ref[keep], eps_keep, w.U0)
+    assert int(keep[kstar]) == kk
+    U = torch.tensor(w.U0, device="cuda")
+    g.optimize(w.x0, U, w.seed, 0)
+    assert any("epi_combine" in n for n in g.last_kernels())
+    du = np.max(np.abs(U.cpu().numpy().astype(np.float64) - Uo))
+    print("PARITY C5 coupled U (oracle costs, %d kept weights): max |dU| %.3g" % (keep.size, du))
+    assert du <= 1e-5
