@@ -915,6 +915,10 @@ __global__ void __launch_bounds__(256) epi_combine_kernel(const EpiCombineArgs a
     if (o > a.TM) return;
     const int idx = o < a.TM ? o : a.TM + 1;
     float acc = 0.0f;
+#ifndef MPPI_COMBINE_UNROLL
+#define MPPI_COMBINE_UNROLL 32   // C5: 113 us (no unroll), 42 (16), 31 (32); profiles/r2_ab_combine_unroll.txt
+#endif
+    MPPI_UNROLL_(MPPI_COMBINE_UNROLL)   // independent loads in flight; the fma chain keeps CTA order
     for (int c = c0; c < c1; ++c) acc = fmaf(sc[c - c0], __ldg(a.epi_part + (size_t)c * stride + idx), acc);
     if (o < a.TM) a.part[(size_t)chunk * a.TM + o] = acc;
     else a.eta_part[chunk] = acc;
