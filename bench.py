@@ -76,17 +76,19 @@ def variant_of(kernels):
     rollout_kernel<Plant, DIAG, NP, GEN, QSTEP> -> "scalar[-grid][-fused][-general][-ctg]:<plant>"."""
     import re
     for k in kernels:
-        mt = re.search(r"rollout_kernel_x2IL(in?)(\d+)ELb([01])ELb([01])ELb([01])ELb([01])E", k)
+        mt = re.search(r"rollout_kernel_x2(s?)IL(in?)(\d+)ELb([01])ELb([01])ELb([01])ELb([01])E", k)
         if mt:
-            np_ = -int(mt.group(2)) if mt.group(1) == "in" else int(mt.group(2))
-            gen, qstep, diag, epi = (mt.group(i) == "1" for i in range(3, 7))
+            vs = mt.group(1) == "s"
+            np_ = -int(mt.group(3)) if mt.group(2) == "in" else int(mt.group(3))
+            gen, qstep, diag, epi = (mt.group(i) == "1" for i in range(4, 8))
         else:
-            mt = re.search(r"rollout_kernel_x2<\s*%s,\s*%s,\s*%s,\s*%s,\s*%s\s*>" % (_I, _B, _B, _B, _B), k)
+            mt = re.search(r"rollout_kernel_x2(s?)<\s*%s,\s*%s,\s*%s,\s*%s,\s*%s\s*>" % (_I, _B, _B, _B, _B), k)
             if mt:
-                np_ = int(mt.group(1))
-                gen, qstep, diag, epi = (_b(mt.group(i)) for i in range(2, 6))
-        if mt:
-            return ("x2" + ("-grid" if np_ == -2 else "") + ("-fused" if gen else "") +
+                vs = mt.group(1) == "s"
+                np_ = int(mt.group(2))
+                gen, qstep, diag, epi = (_b(mt.group(i)) for i in range(3, 7))
+        if mt:   # rollout_kernel_x2s: the small-K kernel (vector-load prologue), same per-step work
+            return ("x2" + ("s" if vs else "") + ("-grid" if np_ == -2 else "") + ("-fused" if gen else "") +
                     ("" if diag else "-general") + ("-ctg" if qstep else "") + ("-epi" if epi else ""))
         mt = re.search(r"rollout_kernelINS_\d+([A-Za-z]+)(?:I.*?E)?ELb([01])EL(in?)(\d+)ELb([01])ELb([01])E", k)
         if mt:
@@ -125,7 +127,9 @@ def rollout_variant(w, K_loc, fused_reduction=True, m=None):
         if v is not None:
             return v
     if w.plant == "quadrotor" and K_loc >= 65536 and w.obstacles is not None and len(w.obstacles) >= 2:
-        return "x2-grid-fused-epi" if fused_reduction else "x2-grid-fused"
+        if not fused_reduction:
+            return "x2-grid-fused"
+        return "x2s-grid-fused-epi" if K_loc < (1 << 19) else "x2-grid-fused-epi"
     return "scalar"
 
 SM_COUNT_B200 = 148

@@ -486,9 +486,14 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
 // tile (written moments ago) to form eta_c and A_c[t][j]; the HBM stream of that read overlaps
 // the other CTAs' ALU-bound rollouts instead of running as a separate pass.  epi_combine_kernel
 // rescales by exp(-(m_c - S_min)/lambda) (the online-softmax identity) in a fixed order.
-template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true, bool EPI = false>
-__global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
-    rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
+//
+// VS (small K): the prologue stages the obstacle-cell table with 16-byte loads, several in flight
+// per thread.  With few CTAs per SM nothing hides the 45 dependent load/store pairs per thread of
+// the plain copy (-4.5 % at K = 2^16); at large K the plain copy's register allocation of the
+// step loop is the faster one (+0.6 % at 2^22), hence a separate kernel (rollout_kernel_x2s)
+// chosen below kVStageMaxK (profiles/r2_ab_cell_staging.txt).
+template <int NP, bool GEN, bool QSTEP, bool DIAG, bool EPI, bool VS>
+__device__ __forceinline__ void rollout_x2_body(const RolloutArgs<QuadrotorParams>& a) {
     constexpr int M = 4;
     extern __shared__ float4 smem4[];
     float4* sObs = smem4;
@@ -513,7 +518,20 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
             sCentXY[kCellMaxCent + i] = c.y;
         }
         const int nc = a.cell_nx * a.cell_ny;
-        for (int i = tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
+        if constexpr (VS) {
+            if (((reinterpret_cast<uintptr_t>(sCells) | reinterpret_cast<uintptr_t>(a.cells)) & 15) == 0) {
+                const int n4 = nc >> 2;
+                const uint4* src = reinterpret_cast<const uint4*>(a.cells);
+                uint4* dst = reinterpret_cast<uint4*>(sCells);
+#pragma unroll 4
+                for (int i = tid; i < n4; i += blockDim.x) dst[i] = __ldg(src + i);
+                for (int i = 4 * n4 + tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
+            } else {
+                for (int i = tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
+            }
+        } else {
+            for (int i = tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
+        }
     }
     if constexpr (DIAG) {
         for (int t = tid; t < a.T; t += blockDim.x) {
@@ -887,6 +905,17 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
             part[a.T * M + 1] = eta;
         }
     }
+}
+
+template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true, bool EPI = false>
+__global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
+    rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
+    rollout_x2_body<NP, GEN, QSTEP, DIAG, EPI, false>(a);
+}
+template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true, bool EPI = false>
+__global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
+    rollout_kernel_x2s(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
+    rollout_x2_body<NP, GEN, QSTEP, DIAG, EPI, true>(a);
 }
 
 // EPI combine: the per-CTA partials of rollout_kernel_x2<..., EPI> rescaled to the global minimum
@@ -2076,7 +2105,8 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
                 if (c.epi_active && c.gen_eps) {    // fused reduction (EPI)
                     a.epi_part = c.d_epi;
                     a.lambda = c.lambda;
-                    kern = (const void*)rollout_kernel_x2<NP, true, false, true, true>;
+                    kern = c.K_loc < kVStageMaxK ? (const void*)rollout_kernel_x2s<NP, true, false, true, true>
+                                                 : (const void*)rollout_kernel_x2<NP, true, false, true, true>;
                 } else {
                     kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
                 }

@@ -37,6 +37,8 @@ def test_variant_of_scalar_and_empty():
     # ncu's demangled names (the roofline-constant captures) parse to the same variants
     assert bench.variant_of(["void mppi::rollout_kernel<mppi::Racecar, true, 1, true, false>(x)"]) == "scalar-fused:racecar"
     assert bench.variant_of(["void mppi::rollout_kernel_x2<(int)-2, 1, 0, 1, 1>(x)"]) == "x2-grid-fused-epi"
+    assert bench.variant_of(["void mppi::rollout_kernel_x2s<(int)-2, 1, 0, 1, 1>(x)"]) == "x2s-grid-fused-epi"
+    assert bench.variant_of([X2.replace("rollout_kernel_x2IL", "rollout_kernel_x2sIL") % ("in2", 1, 0, 1, 1)]) == "x2s-grid-fused-epi"
     assert bench.variant_of([]) is None
     assert bench.variant_of(["_ZN4mppi15finalize_kernelENS_12FinalizeArgsE"]) is None
 
