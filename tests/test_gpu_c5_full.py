@@ -164,3 +164,28 @@ def test_nan_injection_on_packed_path():
     keep = np.setdiff1d(np.arange(K), hit)
     assert np.array_equal(a[keep].view(np.uint32), b[keep].view(np.uint32))
     assert key_k(key2) == k0
+
+
+@pytest.mark.parametrize("K", [65536, 262144 + 4])
+def test_small_k_kernel_agrees_with_the_c5_kernel(oracle, K):
+    """Below K_loc = 2^19 the optimise step runs rollout_kernel_x2s (the C5 kernel's body with a
+    vector-load prologue): its minimum cost and k* are bitwise those of the C5
+    kernel's rollout of the same noise (mppi_rollout_costs), and its update equals the separate
+    reduction's to rounding."""
+    from paper_1509_01149_b200 import _capi as A
+    w = get("C4")
+    m = from_workload(w, K=K)
+    U = cuda_u(w)
+    m.optimize(w.x0, U, 3, 1)
+    assert any("rollout_kernel_x2s" in n for n in m.last_kernels()), m.last_kernels()
+    st = m.stats()
+    c, key = m.rollout_costs(w.x0, cuda_u(w), 3, 1)
+    assert not any("rollout_kernel_x2s" in n for n in m.last_kernels())
+    cn = c.cpu().numpy()
+    assert st["k_star"] == key_k(key) == int(np.argmin(cn))
+    assert np.float32(st["s_min"]).view(np.uint32) == cn.min().view(np.uint32)
+    sep = from_workload(w, K=K)
+    sep.set_option(A.MPPI_OPTION_FUSED_REDUCTION, 0)
+    U2 = cuda_u(w)
+    sep.optimize(w.x0, U2, 3, 1)
+    assert np.max(np.abs(U.cpu().numpy() - U2.cpu().numpy())) <= 1e-6
