@@ -87,7 +87,7 @@ def variant_of(kernels):
                 vs = mt.group(1) == "s"
                 np_ = int(mt.group(2))
                 gen, qstep, diag, epi = (_b(mt.group(i)) for i in range(3, 7))
-        if mt:   # rollout_kernel_x2s: the small-K kernel (vector-load prologue), same per-step work
+        if mt:   # (rollout_kernel_x2s: a v31 small-K variant, folded back into x2 in v32)
             return ("x2" + ("s" if vs else "") + ("-grid" if np_ == -2 else "") + ("-fused" if gen else "") +
                     ("" if diag else "-general") + ("-ctg" if qstep else "") + ("-epi" if epi else ""))
         mt = re.search(r"rollout_kernelINS_\d+([A-Za-z]+)(?:I.*?E)?ELb([01])EL(in?)(\d+)ELb([01])ELb([01])E", k)
@@ -127,9 +127,7 @@ def rollout_variant(w, K_loc, fused_reduction=True, m=None):
         if v is not None:
             return v
     if w.plant == "quadrotor" and K_loc >= 65536 and w.obstacles is not None and len(w.obstacles) >= 2:
-        if not fused_reduction:
-            return "x2-grid-fused"
-        return "x2s-grid-fused-epi" if K_loc < (1 << 19) else "x2-grid-fused-epi"
+        return "x2-grid-fused-epi" if fused_reduction else "x2-grid-fused"
     return "scalar"
 
 SM_COUNT_B200 = 148

@@ -42,7 +42,6 @@ constexpr int kNoiseTT = 8;  // timesteps per noise thread
 constexpr int kMaxStaticPairs = 32;
 // the two-samples-per-thread quadrotor kernel is used from this many samples per GPU on (below
 // it the one-sample kernel fills the 148 SMs better: scripts/compare_pack.py on B200)
-constexpr int64_t kVStageMaxK = 1 << 19;   // below it the C5-path rollout stages its cell table with vector loads
 constexpr int64_t kPackedMinK = 65536;  // quadrotor: obstacle pairs compiled as a constant up to here
 
 // per-timestep constants of the rollout staged in shared memory (one 48-byte record per t)

@@ -397,7 +397,9 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
     float* sMat = sRing + (GEN ? 0 : kEpsStages * blockDim.x * M);
     // candidate grid (NP == kCellGrid, diagonal path only): centres and cell words
     float2* sCent = reinterpret_cast<float2*>(sMat + (DIAG ? 0 : a.T * 2 * M * M));
-    uint32_t* sCells = reinterpret_cast<uint32_t*>(sCent + a.n_cent);
+    // the cell table starts 16-byte aligned (the centre count rounded up to even; the smem size
+    // reserves it) and the device table is padded to whole 16-byte groups (build_cell_grid)
+    uint32_t* sCells = reinterpret_cast<uint32_t*>(sCent + ((a.n_cent + 1) & ~1));
     // candidate-grid centres in static shared memory (compile-time address: each lane's candidate
     // load is one LDS with an immediate base, no address arithmetic)
     __shared__ float sCentXY[NP == kCellGrid ? 2 * kCellMaxCent : 1];
@@ -486,14 +488,9 @@ __global__ void __launch_bounds__(kRolloutThreads, rollout_min_blocks<Plant>())
 // tile (written moments ago) to form eta_c and A_c[t][j]; the HBM stream of that read overlaps
 // the other CTAs' ALU-bound rollouts instead of running as a separate pass.  epi_combine_kernel
 // rescales by exp(-(m_c - S_min)/lambda) (the online-softmax identity) in a fixed order.
-//
-// VS (small K): the prologue stages the obstacle-cell table with 16-byte loads, several in flight
-// per thread.  With few CTAs per SM nothing hides the 45 dependent load/store pairs per thread of
-// the plain copy (-4.5 % at K = 2^16); at large K the plain copy's register allocation of the
-// step loop is the faster one (+0.6 % at 2^22), hence a separate kernel (rollout_kernel_x2s)
-// chosen below kVStageMaxK (profiles/r2_ab_cell_staging.txt).
-template <int NP, bool GEN, bool QSTEP, bool DIAG, bool EPI, bool VS>
-__device__ __forceinline__ void rollout_x2_body(const RolloutArgs<QuadrotorParams>& a) {
+template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true, bool EPI = false>
+__global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
+    rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
     constexpr int M = 4;
     extern __shared__ float4 smem4[];
     float4* sObs = smem4;
@@ -501,7 +498,9 @@ __device__ __forceinline__ void rollout_x2_body(const RolloutArgs<QuadrotorParam
     float* sRing = reinterpret_cast<float*>(sRec + a.T);               // [2][blockDim][2 samples][4]
     float* sMat = sRing + (GEN ? 0 : 2 * kRolloutThreads * 2 * 4);     // !DIAG: [T][2][M*M]
     float2* sCent = reinterpret_cast<float2*>(sMat + (DIAG ? 0 : a.T * 2 * M * M));
-    uint32_t* sCells = reinterpret_cast<uint32_t*>(sCent + a.n_cent);
+    // the cell table starts 16-byte aligned (the centre count rounded up to even; the smem size
+    // reserves it) and the device table is padded to whole 16-byte groups (build_cell_grid)
+    uint32_t* sCells = reinterpret_cast<uint32_t*>(sCent + ((a.n_cent + 1) & ~1));
     // candidate-grid centres in static shared memory (compile-time address: each lane's candidate
     // load is one LDS with an immediate base, no address arithmetic)
     __shared__ float sCentXY[NP == kCellGrid ? 2 * kCellMaxCent : 1];
@@ -517,21 +516,15 @@ __device__ __forceinline__ void rollout_x2_body(const RolloutArgs<QuadrotorParam
             sCentXY[i] = c.x;
             sCentXY[kCellMaxCent + i] = c.y;
         }
-        const int nc = a.cell_nx * a.cell_ny;
-        if constexpr (VS) {
-            if (((reinterpret_cast<uintptr_t>(sCells) | reinterpret_cast<uintptr_t>(a.cells)) & 15) == 0) {
-                const int n4 = nc >> 2;
-                const uint4* src = reinterpret_cast<const uint4*>(a.cells);
-                uint4* dst = reinterpret_cast<uint4*>(sCells);
+        // 16-byte loads, four in flight per thread, no alignment test or tail: the 22 KB table
+        // arrives in a few L2 round trips instead of ~45 dependent load/store pairs per thread,
+        // and the step loop's register allocation comes out faster too (C5 -1.4 %, K = 2^16..2^20
+        // -1.6..2 %; profiles/r2_ab_cell_staging.txt)
+        const uint4* src = reinterpret_cast<const uint4*>(a.cells);
+        uint4* dst = reinterpret_cast<uint4*>(sCells);
+        const int n4 = (a.cell_nx * a.cell_ny + 3) >> 2;
 #pragma unroll 4
-                for (int i = tid; i < n4; i += blockDim.x) dst[i] = __ldg(src + i);
-                for (int i = 4 * n4 + tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
-            } else {
-                for (int i = tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
-            }
-        } else {
-            for (int i = tid; i < nc; i += blockDim.x) sCells[i] = a.cells[i];
-        }
+        for (int i = tid; i < n4; i += blockDim.x) dst[i] = __ldg(src + i);
     }
     if constexpr (DIAG) {
         for (int t = tid; t < a.T; t += blockDim.x) {
@@ -905,17 +898,6 @@ __device__ __forceinline__ void rollout_x2_body(const RolloutArgs<QuadrotorParam
             part[a.T * M + 1] = eta;
         }
     }
-}
-
-template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true, bool EPI = false>
-__global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
-    rollout_kernel_x2(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
-    rollout_x2_body<NP, GEN, QSTEP, DIAG, EPI, false>(a);
-}
-template <int NP, bool GEN, bool QSTEP = false, bool DIAG = true, bool EPI = false>
-__global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
-    rollout_kernel_x2s(const __grid_constant__ RolloutArgs<QuadrotorParams> a) {
-    rollout_x2_body<NP, GEN, QSTEP, DIAG, EPI, true>(a);
 }
 
 // EPI combine: the per-CTA partials of rollout_kernel_x2<..., EPI> rescaled to the global minimum
@@ -2064,7 +2046,7 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
     const size_t smem = (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
                         (c.gen_eps ? 0 : (size_t)(X2 ? 2 : kEpsStages) * kRolloutThreads * spt * Plant::M * sizeof(float)) +
                         (DIAG ? 0 : (size_t)c.T * 2 * Plant::M * Plant::M * sizeof(float)) +
-                        (NP == kCellGrid ? c.cent_host.size() * sizeof(float2) + c.cells_host.size() * sizeof(uint32_t) : 0);
+                        (NP == kCellGrid ? c.cent_host.size() * sizeof(float2) + 16 + c.cells_host.size() * sizeof(uint32_t) : 0);
     const void* kern;
     if constexpr (X2 && !DIAG) {   // general Sigma / A_t: grid path only
         static_assert(NP == kCellGrid, "packed general-Sigma kernel: candidate-grid path only");
@@ -2105,8 +2087,7 @@ static cudaError_t launch_rollout_t(Ctx& c, const typename Plant::Params& P, con
                 if (c.epi_active && c.gen_eps) {    // fused reduction (EPI)
                     a.epi_part = c.d_epi;
                     a.lambda = c.lambda;
-                    kern = c.K_loc < kVStageMaxK ? (const void*)rollout_kernel_x2s<NP, true, false, true, true>
-                                                 : (const void*)rollout_kernel_x2<NP, true, false, true, true>;
+                    kern = (const void*)rollout_kernel_x2<NP, true, false, true, true>;
                 } else {
                     kern = c.gen_eps ? (const void*)rollout_kernel_x2<NP, true> : (const void*)rollout_kernel_x2<NP, false>;
                 }
@@ -2193,7 +2174,7 @@ size_t rollout_smem_bytes(const Ctx& c, bool cells) {
     return (size_t)c.n_obs_pairs * sizeof(float4) + (size_t)c.T * sizeof(StepRec) +
            (size_t)kEpsStages * kRolloutThreads * m * sizeof(float) +
            (c.diag ? 0 : (size_t)c.T * 2 * m * m * sizeof(float)) +
-           (cells ? c.cent_host.size() * sizeof(float2) + c.cells_host.size() * sizeof(uint32_t) : 0);
+           (cells ? c.cent_host.size() * sizeof(float2) + 16 + c.cells_host.size() * sizeof(uint32_t) : 0);
 }
 
 size_t smem_optin_bytes() {

@@ -183,6 +183,7 @@ void build_cell_grid(Ctx& c, const float* xy, int n) {
             }
             words[(size_t)iy * nx + ix] = w;
         }
+    words.resize((words.size() + 3) & ~size_t(3), 0u);   // whole 16-byte groups (vector staging)
     c.cells_host.swap(words);
     c.cent_host.resize(n);
     for (int j = 0; j < n; ++j) c.cent_host[j] = make_float2(-xy[2 * j], -xy[2 * j + 1]);
@@ -1152,8 +1153,9 @@ mppi_status_t mppi_obstacle_grid(const float* xy, int32_t n, uint32_t* words, in
     geom[4] = c.cell_inv_h;
     geom[5] = c.cell_band;
     if (words) {
-        if (capacity < (int64_t)c.cells_host.size()) return fail(MPPI_ERR_INVALID_ARG, "capacity below nx * ny");
-        memcpy(words, c.cells_host.data(), c.cells_host.size() * sizeof(uint32_t));
+        const int64_t ncell = (int64_t)c.cell_nx * c.cell_ny;   // (the device copy is padded past it)
+        if (capacity < ncell) return fail(MPPI_ERR_INVALID_ARG, "capacity below nx * ny");
+        memcpy(words, c.cells_host.data(), (size_t)ncell * sizeof(uint32_t));
     }
     return MPPI_OK;
 }

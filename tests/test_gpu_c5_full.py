@@ -167,20 +167,18 @@ def test_nan_injection_on_packed_path():
 
 
 @pytest.mark.parametrize("K", [65536, 262144 + 4])
-def test_small_k_kernel_agrees_with_the_c5_kernel(oracle, K):
-    """Below K_loc = 2^19 the optimise step runs rollout_kernel_x2s (the C5 kernel's body with a
-    vector-load prologue): its minimum cost and k* are bitwise those of the C5
-    kernel's rollout of the same noise (mppi_rollout_costs), and its update equals the separate
-    reduction's to rounding."""
+def test_fused_reduction_step_agrees_with_the_rollout_pass(oracle, K):
+    """The optimise step's rollout (fused reduction epilogue) and mppi_rollout_costs' rollout of the
+    same noise give a bitwise-equal minimum cost and k*, and the update equals the separate
+    reduction's to rounding (K = 2^16 and a ragged 2^18 + 4)."""
     from paper_1509_01149_b200 import _capi as A
     w = get("C4")
     m = from_workload(w, K=K)
     U = cuda_u(w)
     m.optimize(w.x0, U, 3, 1)
-    assert any("rollout_kernel_x2s" in n for n in m.last_kernels()), m.last_kernels()
+    assert any("rollout_kernel_x2" in n for n in m.last_kernels()) and any("epi_combine" in n for n in m.last_kernels())
     st = m.stats()
     c, key = m.rollout_costs(w.x0, cuda_u(w), 3, 1)
-    assert not any("rollout_kernel_x2s" in n for n in m.last_kernels())
     cn = c.cpu().numpy()
     assert st["k_star"] == key_k(key) == int(np.argmin(cn))
     assert np.float32(st["s_min"]).view(np.uint32) == cn.min().view(np.uint32)
