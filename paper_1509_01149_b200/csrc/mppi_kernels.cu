@@ -516,14 +516,14 @@ __global__ void __launch_bounds__(kRolloutThreads, MPPI_X2_MINB)
             sCentXY[i] = c.x;
             sCentXY[kCellMaxCent + i] = c.y;
         }
-        // 16-byte loads, four in flight per thread, no alignment test or tail: the 22 KB table
+        // 16-byte loads, eight in flight per thread, no alignment test or tail: the 22 KB table
         // arrives in a few L2 round trips instead of ~45 dependent load/store pairs per thread,
         // and the step loop's register allocation comes out faster too (C5 -1.4 %, K = 2^16..2^20
         // -1.6..2 %; profiles/r2_ab_cell_staging.txt)
         const uint4* src = reinterpret_cast<const uint4*>(a.cells);
         uint4* dst = reinterpret_cast<uint4*>(sCells);
         const int n4 = (a.cell_nx * a.cell_ny + 3) >> 2;
-#pragma unroll 4
+#pragma unroll 8   // (4: +0.2 % at C5, profiles/r2_ab_cell_staging.txt)
         for (int i = tid; i < n4; i += blockDim.x) dst[i] = __ldg(src + i);
     }
     if constexpr (DIAG) {
